@@ -1,0 +1,349 @@
+"""Benchmark of the RICI hot path (arXiv 2007.02306) on B200.
+
+One step = one pass of the whole hot path over the C2 workload (BASELINE.json configs[1]):
+  a1     rici_create_mesh   bumpy torus 264x132, T=69,696 triangles
+  a2-a8  rici_generate      RICI 64x64 at all V=34,848 vertices, R=0.3
+  a9-a12 rici_crss_search   every image as a needle against all images (self-search,
+                            correspondence i <-> i): 34,848^2 = 1.21e9 CRSS comparisons
+value = images (generated and ranked) per second for the whole job.  At N>1 GPUs (weak
+scaling) each rank adds its own C2-sized object: rank r generates object r's images (its
+haystack shard); the needles are rank 0's images (broadcast); thresholds and counts are
+all-reduced over NCCL (paper_2007_02306_b200.dist).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "RICI images/s (64x64) and CRSS comparisons/s at 1/2/4/8 B200; % roofline"
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+SMS = 148
+LANES_PER_SM = 128          # FP32/INT32 lanes per SM
+CRSS_OPS_PER_TERM = 3       # D_h difference, (D_n - D_h), multiply-accumulate
+
+
+def peaks():
+    try:
+        with open(PEAKS_PATH) as f:
+            p = json.load(f)
+        return p, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            parts = [p.strip() for p in l.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- workload
+def workload(rank: int):
+    import synth
+    cfg = synth.config_c2() if rank == 0 else {
+        **synth.config_c2(), "mesh": synth.bumpy_torus(264, 132, key=(2, rank, 0))}
+    if rank != 0:
+        cfg["origins"] = cfg["mesh"].origins
+    return cfg
+
+
+def cpu_baseline(cfg, budget_s: float = 20.0):
+    """The oracle as it stands on a bounded sample of the C2 step: generate a sample of the
+    images and run CRSS of sampled needles against a sample of the haystack; extrapolate the
+    step's time (n * t_image + n^2 * t_comparison) and report images/s of the step."""
+    import oracle
+    m = cfg["mesh"]
+    n = m.n_vertices
+    rng = np.random.default_rng(0)
+    k_img = 512
+    idx = np.sort(rng.choice(n, k_img, replace=False))
+    t0 = time.perf_counter()
+    imgs = oracle.rici_generate(m.vertices, m.indices, cfg["origins"][idx], cfg["R"], cfg["N"])["images"]
+    t_gen = time.perf_counter() - t0
+    per_img = t_gen / k_img
+    # CRSS: needles x haystack from the generated sample (the oracle's dense loop cost is
+    # data independent); scale the pair count to ~budget/2 seconds
+    nn_s, nh_s = 32, k_img
+    t0 = time.perf_counter()
+    oracle.crss_matrix(imgs[:nn_s], imgs[:nh_s])
+    t_c = time.perf_counter() - t0
+    reps = max(1, int((budget_s / 2) / max(t_c, 1e-3)))
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        oracle.crss_matrix(imgs[:nn_s], imgs[:nh_s])
+    t_c = (time.perf_counter() - t0) / reps
+    per_cmp = t_c / (nn_s * nh_s)
+    t_step = n * per_img + float(n) * n * per_cmp
+    return {"value": n / t_step, "unit": "images/s", "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": (f"oracle rici_generate of {k_img} sampled C2 images ({t_gen:.2f} s) + "
+                       f"{reps}x oracle CRSS {nn_s}x{nh_s} ({t_c:.3f} s each); step time "
+                       f"extrapolated as n*t_image + n^2*t_comparison for n={n}"),
+            "t_image_s": per_img, "t_comparison_s": per_cmp, "t_step_s": t_step}
+
+
+def run_reference(args):
+    """--impl reference: the oracle timed as it stands on the host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = workload(0)
+    n = cfg["mesh"].n_vertices
+    for _ in range(args.warmup):
+        cpu_baseline(cfg, budget_s=2.0)
+    vals = []
+    cb = None
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        cb = cpu_baseline(cfg, budget_s=6.0)
+        vals.append(cb["t_step_s"])
+    wall = time.perf_counter() - t0
+    t_step = float(np.mean(vals))
+    value = n / t_step
+    cbl = {k: cb[k] for k in ("unit", "cores", "kind", "sample")}
+    cbl["value"] = value
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "images/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64/i64", "data": "synthetic",
+            "config": {"workload": "C2: bumpy torus 264x132 (T=69,696), RICI 64x64 at all 34,848 "
+                                   "vertices, R=0.3, CRSS self-search 34,848 x 34,848",
+                       "bench_wall_s": wall},
+            "cpu_baseline": cbl,
+            "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2007_02306_b200 as rici
+    from paper_2007_02306_b200 import dist as rdist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    rici._lib.load()
+
+    cfg = workload(rank)
+    m = cfg["mesh"]
+    R, N = cfg["R"], cfg["N"]
+    n = m.n_vertices
+    v_d = torch.from_numpy(m.vertices).to(dev)
+    t_d = torch.from_numpy(m.indices).to(dev)
+    o_d = torch.from_numpy(cfg["origins"]).to(dev)
+    imgs = torch.empty((n, N, N), dtype=torch.int16, device=dev)
+    needles = torch.empty((workload(0)["mesh"].n_vertices if world > 1 else n, N, N), dtype=torch.int16, device=dev)
+    ranks_d = torch.empty(n, dtype=torch.int32, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > L2 (126 MB)
+    stream = torch.cuda.current_stream()
+
+    ev = {k: [] for k in ("step", "gen", "crss")}
+
+    def step(record: bool):
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        e[0].record(stream)
+        mesh = rici.rici_create_mesh(v_d, t_d)
+        e[1].record(stream)
+        rici.rici_generate(mesh, o_d, R, N, out=imgs)
+        e[2].record(stream)
+        if world == 1:
+            rici.rici_crss_search(imgs, imgs, out=ranks_d)
+        else:
+            if rank == 0:
+                needles.copy_(imgs)
+            dist.broadcast(needles, 0)
+            rdist.search_sharded(needles, imgs, rank * n, N)
+        e[3].record(stream)
+        mesh.destroy()
+        if record:
+            ev["step"].append((e[0], e[3]))
+            ev["gen"].append((e[1], e[2]))
+            ev["crss"].append((e[2], e[3]))
+
+    for _ in range(max(args.warmup, 0)):
+        step(False)
+        flush.zero_()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches0 = rici.rici_launch_count()
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            step(True)
+            flush.zero_()                      # L2 flush between timed steps (outside the events)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        wall = time.perf_counter() - t0
+    launches = rici.rici_launch_count() - launches0
+
+    def ms(k):
+        return float(np.mean([a.elapsed_time(b) for a, b in ev[k]]))
+
+    step_ms, gen_ms, crss_ms = ms("step"), ms("gen"), ms("crss")
+    step_ms_max = step_ms
+    if world > 1:
+        t = torch.tensor([step_ms, gen_ms, crss_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        step_ms_max, gen_ms, crss_ms = [float(x) for x in t.cpu()]
+
+    # ---- end-to-end through the public API with HOST buffers (rank 0, N=1 only)
+    e2e = None
+    if world == 1:
+        vh = torch.from_numpy(m.vertices).pin_memory()
+        th = torch.from_numpy(m.indices).pin_memory()
+        oh = torch.from_numpy(cfg["origins"]).pin_memory()
+        rh = torch.empty(n, dtype=torch.int32).pin_memory()
+
+        def e2e_step():
+            mesh = rici.rici_create_mesh(vh, th)                     # H2D inside the library
+            rici.rici_generate(mesh, oh, R, N, out=imgs)             # origins H2D inside
+            rici.rici_crss_search(imgs, imgs, out=rh)                # ranks D2H + sync inside
+            mesh.destroy()
+        for _ in range(2):
+            e2e_step()
+            flush.zero_()
+        torch.cuda.synchronize()
+        tt = []
+        for _ in range(args.steps):
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            e2e_step()
+            tt.append(time.perf_counter() - t1)
+            flush.zero_()
+        torch.cuda.synchronize()
+        e2e = {"value": n / float(np.mean(tt)), "unit": "images/s",
+               "h2d_bytes_per_step": int(vh.numel() * 4 + th.numel() * 4 + oh.numel() * 4),
+               "d2h_bytes_per_step": int(rh.numel() * 4), "ms_per_step": float(np.mean(tt)) * 1e3}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel (CRSS count kernel: integer ALU bound)
+    pk, src = peaks()
+    sm_mhz = pk.get("sm_max_mhz", 1965.0)
+    imgs_np = imgs.cpu().numpy().view(np.uint16)
+    d = np.diff(imgs_np.astype(np.int32), axis=2)
+    nnz = int((d != 0).sum())                                 # sum over needles of |mask|
+    n_total_hay = n * world
+    terms = float(nnz) * n_total_hay / world                  # per rank: every needle x local shard
+    comparisons = float(imgs_np.shape[0]) * n                # per rank
+    crss_s = crss_ms / 1e3
+    achieved = terms * CRSS_OPS_PER_TERM / crss_s / 1e12      # Tops/s
+    peak = SMS * LANES_PER_SM * sm_mhz * 1e6 / 1e12
+    roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s",
+            "frac": achieved / peak, "traffic": None,
+            "kernel": "crss_tile_kernel (+needle prepare, thresholds; timed as the rici_crss_search call)",
+            "peak_source": f"{SMS} SMs x {LANES_PER_SM} INT32 lanes x sm_max {sm_mhz} MHz ({src} clock)",
+            "algorithmic": f"{CRSS_OPS_PER_TERM} int ops per masked term; {nnz} masked needle terms "
+                           f"x {n} haystack images per rank",
+            "hbm_equivalent_frac": comparisons * 8192 / crss_s / 1e9 / pk.get("hbm_gbs", 6548.8)}
+    images_per_s = n_total_hay / (step_ms_max / 1e3)
+    cb = cpu_baseline(cfg) if world == 1 and not args.no_cpu_baseline else None
+    line = {"metric": METRIC, "value": images_per_s, "unit": "images/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms_max,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32/i32",
+            "data": "synthetic",
+            "config": {"workload": "C2: bumpy torus 264x132 (T=69,696), RICI 64x64 at all 34,848 "
+                                   "vertices, R=0.3, CRSS self-search 34,848 x 34,848"
+                                   + ("" if world == 1 else f"; weak: {world} objects, haystack sharded"),
+                       "images_per_rank": n, "comparisons_per_step": comparisons * world,
+                       "l2": "flushed between timed steps (256 MB write); haystack 285 MB > L2",
+                       "parallelism": f"dp{world}"},
+            "comparisons_per_s": comparisons * world / (step_ms_max / 1e3),
+            "construction": {"ms": gen_ms, "images_per_s": n / (gen_ms / 1e3)},
+            "crss": {"ms": crss_ms, "comparisons_per_s": comparisons / crss_s},
+            "roofline": roof, "cpu_baseline": cb, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clk.summary(), "bench_wall_s": wall}
+    print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="rici", choices=["rici", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,150 @@
+/*
+ * rici.h -- C ABI of the B200-native RICI hot path (arXiv 2007.02306).
+ *
+ * Two steps of the paper's method run behind this boundary, as hand-written
+ * sm_100a CUDA kernels:
+ *   (a) RICI construction   "iterate over each triangle in the scene",
+ *       three steps per triangle: project (Eqs. 1-5),
+ *       per-layer circle/triangle intersection ranges, bin increments.
+ *   (b) CRSS search         the clutter-resistant distance (Eq. 6, Eq. 7
+ *       P:346-348, Listing 1) of every needle against every haystack
+ *       image, and the rank of the true correspondence (best tie P:459).
+ * "P:n" = line n of the paper text; G1..G16 = readings listed in DESIGN.md.
+ *
+ * Conventions for every entry point
+ * ---------------------------------
+ * Pointers.  Every bulk pointer may be CUDA DEVICE memory or HOST memory
+ *   (pinned or pageable); the library inspects it with cudaPointerGetAttributes.
+ *   Host inputs are copied to device workspace on `stream`; host outputs are
+ *   copied back on `stream` and the call then synchronises `stream` before it
+ *   returns.  With device pointers nothing is synchronised (except
+ *   rici_create_mesh, see there).
+ * Ownership.  The caller owns every buffer it passes; the library never frees
+ *   or retains them past the call.  Inputs are never modified.  A rici_mesh
+ *   owns its device triangle buffer until rici_destroy_mesh.
+ * Stream.  All work is enqueued on `stream` (a cudaStream_t; NULL = legacy
+ *   default stream) on the current device.  Outputs on device are valid once
+ *   the stream reaches the point of the call.
+ * Errors.  Each call returns a rici_status.  Argument errors are detected
+ *   synchronously before anything is enqueued (RICI_ERR_INVALID_ARGUMENT).
+ *   CUDA errors return RICI_ERR_CUDA.  A device other than sm_100 returns
+ *   RICI_ERR_UNSUPPORTED.  rici_last_error() gives a message for the last
+ *   failing call on the calling thread.  No exception or abort crosses the ABI.
+ * Images.  A RICI image is n_bins x n_bins uint16, row-major
+ *   [row = beta layer, ascending][column = radius alpha, ascending] (P:117-121,
+ *   G4), counts saturated at 65535 (G9).  2 <= n_bins <= 128 is accepted;
+ *   n_bins = 64 is the paper's setting and the tuned path.
+ */
+#ifndef RICI_H_
+#define RICI_H_
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define RICI_API __attribute__((visibility("default")))
+#else
+#define RICI_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *rici_stream_t;   /* identical to cudaStream_t */
+typedef struct rici_mesh_s *rici_mesh;       /* opaque device triangle buffer */
+
+typedef enum {
+    RICI_OK = 0,
+    RICI_ERR_INVALID_ARGUMENT = 1,
+    RICI_ERR_CUDA = 2,
+    RICI_ERR_OUT_OF_MEMORY = 3,
+    RICI_ERR_UNSUPPORTED = 4
+} rici_status;
+
+/* ---- (a1) mesh staging ----------------------------------------------------
+ * Builds the device triangle buffer the construction kernel streams: every
+ * triangle "in the scene" de-indexed into its three vertex positions
+ * and grouped into spatially compact chunks (an internal reordering that
+ * cannot change any image: counts are sums over triangles).
+ *   vertices   [n_vertices][3] float32 x,y,z
+ *   indices    [n_triangles][3] int32, each in [0, n_vertices)
+ *   out_mesh   receives the handle (unchanged on error)
+ * n_triangles = 0 is a valid empty scene (every image is zero).
+ * Index validation reads the indices, so this call synchronises `stream`;
+ * an out-of-range index returns RICI_ERR_INVALID_ARGUMENT.                   */
+RICI_API rici_status rici_create_mesh(const float *vertices, int64_t n_vertices,
+                             const int32_t *indices, int64_t n_triangles,
+                             rici_stream_t stream, rici_mesh *out_mesh);
+
+/* Frees the mesh (cudaFree: waits for outstanding work on the device).  NULL is a no-op. */
+RICI_API rici_status rici_destroy_mesh(rici_mesh mesh);
+
+/* Number of triangles in the mesh, or -1 for NULL. */
+RICI_API int64_t rici_mesh_num_triangles(rici_mesh mesh);
+
+/* ---- (a2-a8) RICI construction ---------------------------------------------
+ * One RICI per oriented point (spin vertex S_v + spin normal S_n).
+ *   origins        [n][6] float32 (px,py,pz,nx,ny,nz); the normal need not be
+ *                  unit length (it is normalised, G3); a zero or non-finite
+ *                  normal yields an all-zero image (not an error).
+ *   n              >= 0 images
+ *   support_radius R > 0, finite: image width R (alpha in [0,R]) and height R
+ *                  (beta in [-R/2, R/2]) (G4)
+ *   n_bins         N in [2,128]
+ *   out            [n][N][N] uint16, fully overwritten
+ * Arithmetic is FP32 (paper: float kernels, G13); pixels whose circle lies
+ * within ~1e-5*R of a layer/bin/sign decision may differ from an exact
+ * evaluation (the north-star attribution rule).                             */
+RICI_API rici_status rici_generate(rici_mesh mesh, const float *origins, int64_t n,
+                          float support_radius, int32_t n_bins,
+                          uint16_t *out, rici_stream_t stream);
+
+/* ---- (a9-a12) CRSS search ---------------------------------------------------
+ * Rank of each needle's true correspondence with the implicit correspondence
+ * needle i <-> haystack i (G11): rank_i = #{ j : CRSS(n_i,h_j) < CRSS(n_i,h_i) }
+ * (strict, so ties take the best rank; 0 <= rank <= n_haystack-1).
+ *   needles    [n_needles][N][N] uint16
+ *   haystack   [n_haystack][N][N] uint16, n_haystack >= n_needles
+ *   out_ranks  [n_needles] uint32
+ * Exact integer arithmetic (bit-exact for every input).                       */
+RICI_API rici_status rici_crss_search(const uint16_t *needles, int64_t n_needles,
+                             const uint16_t *haystack, int64_t n_haystack,
+                             int32_t n_bins, uint32_t *out_ranks, rici_stream_t stream);
+
+/* Sharding primitives (used by the multi-GPU layer).
+ * rici_crss_pairs: out[k] = CRSS(needles[pairs[k][0]], haystack[pairs[k][1]]).
+ *   pairs [m][2] int64 (needle index, haystack index).  With HOST pairs every
+ *   index is validated (RICI_ERR_INVALID_ARGUMENT); with DEVICE pairs an
+ *   out-of-range pair yields out[k] = UINT64_MAX.                           */
+RICI_API rici_status rici_crss_pairs(const uint16_t *needles, int64_t n_needles,
+                            const uint16_t *haystack, int64_t n_haystack, int32_t n_bins,
+                            const int64_t *pairs, int64_t m, uint64_t *out,
+                            rici_stream_t stream);
+
+/* out_counts[i] = #{ j in [0,n_haystack) : CRSS(needles[i], haystack[j]) < thresholds[i] }
+ * (overwritten, not accumulated).  thresholds [n_needles] uint64.            */
+RICI_API rici_status rici_crss_count_below(const uint16_t *needles, int64_t n_needles,
+                                  const uint16_t *haystack, int64_t n_haystack, int32_t n_bins,
+                                  const uint64_t *thresholds, uint32_t *out_counts,
+                                  rici_stream_t stream);
+
+/* Full distance matrix out[i][j] = CRSS(needles[i], haystack[j]), uint64. */
+RICI_API rici_status rici_crss_distances(const uint16_t *needles, int64_t n_needles,
+                                const uint16_t *haystack, int64_t n_haystack, int32_t n_bins,
+                                uint64_t *out, rici_stream_t stream);
+
+/* ---- diagnostics ------------------------------------------------------------ */
+/* Message of the last failing call on this thread ("" if none).  Valid until
+ * the next rici_* call on this thread. */
+RICI_API const char *rici_last_error(void);
+
+/* Total number of kernels this library has launched in this process. */
+RICI_API uint64_t rici_launch_count(void);
+
+/* "rici-b200 <version> sm_100a" */
+RICI_API const char *rici_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RICI_H_ */

@@ -1,0 +1,350 @@
+// abi.cu -- the C ABI of librici.so (include/rici.h): argument validation, host/device
+// staging, workspace, launch sequencing and error reporting.  No compute happens here.
+#include <atomic>
+#include <cstdarg>
+#include <new>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "rici.h"
+#include "rici_internal.cuh"
+
+struct rici_mesh_s {
+    rici::DeviceMesh m;
+};
+
+namespace rici {
+static std::atomic<unsigned long long> g_launches{0};
+void note_launches(int k) { g_launches.fetch_add((unsigned long long)k, std::memory_order_relaxed); }
+}  // namespace rici
+
+namespace {
+
+thread_local std::string g_err;
+
+rici_status fail(rici_status st, const char *fmt, ...) __attribute__((format(printf, 2, 3)));
+rici_status fail(rici_status st, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+
+rici_status cuda_fail(cudaError_t e, const char *what) {
+    cudaGetLastError();   // clear sticky-free errors
+    if (e == cudaErrorMemoryAllocation)
+        return fail(RICI_ERR_OUT_OF_MEMORY, "%s: %s", what, cudaGetErrorString(e));
+    return fail(RICI_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+// sm_100 only (the kernels are compiled for sm_100a and nothing else).
+rici_status check_device() {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    static int cached[64];
+    static bool init = false;
+    if (!init) { for (int &c : cached) c = -1; init = true; }
+    if (dev >= 0 && dev < 64 && cached[dev] >= 0)
+        return cached[dev] ? RICI_OK : fail(RICI_ERR_UNSUPPORTED, "device %d is not sm_100", dev);
+    int major = 0, minor = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    bool ok = (major == 10 && minor == 0);
+    if (dev >= 0 && dev < 64) cached[dev] = ok ? 1 : 0;
+    if (!ok) return fail(RICI_ERR_UNSUPPORTED, "device %d is sm_%d%d; this build is sm_100a only", dev, major, minor);
+    // keep freed workspace in the stream-ordered pool between calls
+    static bool pool_set[64] = {};
+    if (dev < 64 && !pool_set[dev]) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        pool_set[dev] = true;
+    }
+    return RICI_OK;
+}
+
+bool is_device_ptr(const void *p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return false; }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// Collects stream-ordered temporaries and host write-backs for one call.
+struct Staging {
+    cudaStream_t s;
+    std::vector<void *> temps;
+    struct Back { void *host; const void *dev; size_t bytes; };
+    std::vector<Back> backs;
+    explicit Staging(cudaStream_t st) : s(st) {}
+    ~Staging() { for (void *t : temps) cudaFreeAsync(t, s); }
+
+    cudaError_t in(const void *p, size_t bytes, const void **dev) {
+        if (p == nullptr || bytes == 0 || is_device_ptr(p)) { *dev = p; return cudaSuccess; }
+        void *d = nullptr;
+        cudaError_t e = cudaMallocAsync(&d, bytes, s);
+        if (e != cudaSuccess) return e;
+        temps.push_back(d);
+        *dev = d;
+        return cudaMemcpyAsync(d, p, bytes, cudaMemcpyHostToDevice, s);
+    }
+    cudaError_t out(void *p, size_t bytes, void **dev) {
+        if (p == nullptr || bytes == 0 || is_device_ptr(p)) { *dev = p; return cudaSuccess; }
+        void *d = nullptr;
+        cudaError_t e = cudaMallocAsync(&d, bytes, s);
+        if (e != cudaSuccess) return e;
+        temps.push_back(d);
+        backs.push_back({p, d, bytes});
+        *dev = d;
+        return cudaSuccess;
+    }
+    cudaError_t finish() {
+        if (backs.empty()) return cudaSuccess;
+        for (auto &b : backs) {
+            cudaError_t e = cudaMemcpyAsync(b.host, b.dev, b.bytes, cudaMemcpyDeviceToHost, s);
+            if (e != cudaSuccess) return e;
+        }
+        return cudaStreamSynchronize(s);
+    }
+};
+
+bool valid_bins(int32_t n_bins) { return n_bins >= 2 && n_bins <= 128; }
+
+rici_status check_images(const void *p, int64_t n, const char *name) {
+    if (n < 0) return fail(RICI_ERR_INVALID_ARGUMENT, "%s: negative count %lld", name, (long long)n);
+    if (n > 0 && p == nullptr) return fail(RICI_ERR_INVALID_ARGUMENT, "%s: null pointer", name);
+    return RICI_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *rici_last_error(void) { return g_err.c_str(); }
+
+uint64_t rici_launch_count(void) { return rici::g_launches.load(); }
+
+const char *rici_version(void) { return "rici-b200 0.1.0 sm_100a"; }
+
+int64_t rici_mesh_num_triangles(rici_mesh mesh) { return mesh ? mesh->m.nt : -1; }
+
+rici_status rici_create_mesh(const float *vertices, int64_t n_vertices, const int32_t *indices,
+                             int64_t n_triangles, rici_stream_t stream, rici_mesh *out_mesh) {
+    g_err.clear();
+    if (!out_mesh) return fail(RICI_ERR_INVALID_ARGUMENT, "out_mesh is null");
+    if (n_vertices < 0 || n_triangles < 0)
+        return fail(RICI_ERR_INVALID_ARGUMENT, "negative vertex/triangle count");
+    if (n_triangles > 0 && (!vertices || !indices))
+        return fail(RICI_ERR_INVALID_ARGUMENT, "null vertices/indices");
+    if (n_triangles > 0 && n_vertices == 0)
+        return fail(RICI_ERR_INVALID_ARGUMENT, "triangles given but no vertices");
+    if (rici_status st = check_device()) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    rici_mesh_s *mesh = new (std::nothrow) rici_mesh_s();
+    if (!mesh) return fail(RICI_ERR_OUT_OF_MEMORY, "host allocation failed");
+    cudaGetDevice(&mesh->m.device);
+    int64_t n_chunks = (n_triangles + rici::kChunk - 1) / rici::kChunk;
+    cudaError_t e = cudaSuccess;
+    if (n_chunks > 0) {
+        e = cudaMalloc(&mesh->m.tri, sizeof(float) * 9 * rici::kChunk * (size_t)n_chunks);
+        if (e == cudaSuccess) e = cudaMalloc(&mesh->m.sphere, sizeof(float4) * (size_t)n_chunks);
+        if (e != cudaSuccess) { rici_destroy_mesh(mesh); return cuda_fail(e, "mesh allocation"); }
+        Staging st(s);
+        const void *dv = nullptr, *di = nullptr;
+        int *d_bad = nullptr;
+        if ((e = st.in(vertices, sizeof(float) * 3 * (size_t)n_vertices, &dv)) == cudaSuccess &&
+            (e = st.in(indices, sizeof(int32_t) * 3 * (size_t)n_triangles, &di)) == cudaSuccess &&
+            (e = cudaMallocAsync((void **)&d_bad, sizeof(int), s)) == cudaSuccess) {
+            st.temps.push_back(d_bad);
+            if ((e = cudaMemsetAsync(d_bad, 0, sizeof(int), s)) == cudaSuccess)
+                e = rici::launch_mesh_stage((const float *)dv, n_vertices, (const int32_t *)di,
+                                            n_triangles, &mesh->m, d_bad, s);
+            int bad = 0;
+            if (e == cudaSuccess) e = cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, s);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+            if (e == cudaSuccess && bad) {
+                rici_destroy_mesh(mesh);
+                return fail(RICI_ERR_INVALID_ARGUMENT, "triangle index out of range [0, %lld)",
+                            (long long)n_vertices);
+            }
+        }
+        if (e != cudaSuccess) { rici_destroy_mesh(mesh); return cuda_fail(e, "rici_create_mesh"); }
+    } else {
+        mesh->m.nt = 0;
+        mesh->m.n_chunks = 0;
+    }
+    *out_mesh = mesh;
+    return RICI_OK;
+}
+
+rici_status rici_destroy_mesh(rici_mesh mesh) {
+    g_err.clear();
+    if (!mesh) return RICI_OK;
+    if (mesh->m.tri) cudaFree(mesh->m.tri);
+    if (mesh->m.sphere) cudaFree(mesh->m.sphere);
+    delete mesh;
+    return RICI_OK;
+}
+
+rici_status rici_generate(rici_mesh mesh, const float *origins, int64_t n, float support_radius,
+                          int32_t n_bins, uint16_t *out, rici_stream_t stream) {
+    g_err.clear();
+    if (!mesh) return fail(RICI_ERR_INVALID_ARGUMENT, "mesh is null");
+    if (n < 0) return fail(RICI_ERR_INVALID_ARGUMENT, "negative image count");
+    if (n > 0 && (!origins || !out)) return fail(RICI_ERR_INVALID_ARGUMENT, "null origins/out");
+    if (!(support_radius > 0.f) || !std::isfinite(support_radius))
+        return fail(RICI_ERR_INVALID_ARGUMENT, "support_radius must be finite and > 0");
+    if (!valid_bins(n_bins)) return fail(RICI_ERR_INVALID_ARGUMENT, "n_bins must be in [2,128]");
+    if (rici_status st = check_device()) return st;
+    if (n == 0) return RICI_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    Staging st(s);
+    const void *dorig = nullptr;
+    void *dout = nullptr;
+    size_t out_bytes = sizeof(uint16_t) * (size_t)n * n_bins * n_bins;
+    cudaError_t e = st.in(origins, sizeof(float) * 6 * (size_t)n, &dorig);
+    if (e == cudaSuccess) e = st.out(out, out_bytes, &dout);
+    if (e == cudaSuccess)
+        e = rici::launch_generate(mesh->m, (const float *)dorig, n, support_radius, n_bins,
+                                  (uint16_t *)dout, s);
+    if (e == cudaSuccess) e = st.finish();
+    if (e != cudaSuccess) return cuda_fail(e, "rici_generate");
+    return RICI_OK;
+}
+
+rici_status rici_crss_pairs(const uint16_t *needles, int64_t n_needles, const uint16_t *haystack,
+                            int64_t n_haystack, int32_t n_bins, const int64_t *pairs, int64_t m,
+                            uint64_t *out, rici_stream_t stream) {
+    g_err.clear();
+    if (!valid_bins(n_bins)) return fail(RICI_ERR_INVALID_ARGUMENT, "n_bins must be in [2,128]");
+    if (rici_status st = check_images(needles, n_needles, "needles")) return st;
+    if (rici_status st = check_images(haystack, n_haystack, "haystack")) return st;
+    if (m < 0) return fail(RICI_ERR_INVALID_ARGUMENT, "negative pair count");
+    if (m > 0 && (!pairs || !out)) return fail(RICI_ERR_INVALID_ARGUMENT, "null pairs/out");
+    if (rici_status st = check_device()) return st;
+    if (m == 0) return RICI_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!is_device_ptr(pairs)) {
+        for (int64_t k = 0; k < m; ++k)
+            if (pairs[2 * k] < 0 || pairs[2 * k] >= n_needles || pairs[2 * k + 1] < 0 ||
+                pairs[2 * k + 1] >= n_haystack)
+                return fail(RICI_ERR_INVALID_ARGUMENT, "pair %lld out of range", (long long)k);
+    }
+    const size_t P = (size_t)n_bins * n_bins;
+    Staging st(s);
+    const void *dn = nullptr, *dh = nullptr, *dp = nullptr;
+    void *dout = nullptr;
+    cudaError_t e = st.in(needles, sizeof(uint16_t) * P * n_needles, &dn);
+    if (e == cudaSuccess) e = st.in(haystack, sizeof(uint16_t) * P * n_haystack, &dh);
+    if (e == cudaSuccess) e = st.in(pairs, sizeof(int64_t) * 2 * (size_t)m, &dp);
+    if (e == cudaSuccess) e = st.out(out, sizeof(uint64_t) * (size_t)m, &dout);
+    if (e == cudaSuccess)
+        e = rici::launch_crss_pairs((const uint16_t *)dn, n_needles, (const uint16_t *)dh, n_haystack,
+                                    n_bins, (const int64_t *)dp, m, (uint64_t *)dout, s);
+    if (e == cudaSuccess) e = st.finish();
+    if (e != cudaSuccess) return cuda_fail(e, "rici_crss_pairs");
+    return RICI_OK;
+}
+
+rici_status rici_crss_count_below(const uint16_t *needles, int64_t n_needles,
+                                  const uint16_t *haystack, int64_t n_haystack, int32_t n_bins,
+                                  const uint64_t *thresholds, uint32_t *out_counts,
+                                  rici_stream_t stream) {
+    g_err.clear();
+    if (!valid_bins(n_bins)) return fail(RICI_ERR_INVALID_ARGUMENT, "n_bins must be in [2,128]");
+    if (rici_status st = check_images(needles, n_needles, "needles")) return st;
+    if (rici_status st = check_images(haystack, n_haystack, "haystack")) return st;
+    if (n_needles > 0 && (!thresholds || !out_counts))
+        return fail(RICI_ERR_INVALID_ARGUMENT, "null thresholds/out_counts");
+    if (rici_status st = check_device()) return st;
+    if (n_needles == 0) return RICI_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t P = (size_t)n_bins * n_bins;
+    Staging st(s);
+    const void *dn = nullptr, *dh = nullptr, *dt = nullptr;
+    void *dc = nullptr;
+    cudaError_t e = st.in(needles, sizeof(uint16_t) * P * n_needles, &dn);
+    if (e == cudaSuccess) e = st.in(haystack, sizeof(uint16_t) * P * n_haystack, &dh);
+    if (e == cudaSuccess) e = st.in(thresholds, sizeof(uint64_t) * (size_t)n_needles, &dt);
+    if (e == cudaSuccess) e = st.out(out_counts, sizeof(uint32_t) * (size_t)n_needles, &dc);
+    if (e == cudaSuccess)
+        e = rici::launch_crss_search_tiles((const uint16_t *)dn, n_needles, (const uint16_t *)dh,
+                                           n_haystack, n_bins, (const uint64_t *)dt, (uint32_t *)dc,
+                                           nullptr, s);
+    if (e == cudaSuccess) e = st.finish();
+    if (e != cudaSuccess) return cuda_fail(e, "rici_crss_count_below");
+    return RICI_OK;
+}
+
+rici_status rici_crss_distances(const uint16_t *needles, int64_t n_needles,
+                                const uint16_t *haystack, int64_t n_haystack, int32_t n_bins,
+                                uint64_t *out, rici_stream_t stream) {
+    g_err.clear();
+    if (!valid_bins(n_bins)) return fail(RICI_ERR_INVALID_ARGUMENT, "n_bins must be in [2,128]");
+    if (rici_status st = check_images(needles, n_needles, "needles")) return st;
+    if (rici_status st = check_images(haystack, n_haystack, "haystack")) return st;
+    if (n_needles > 0 && n_haystack > 0 && !out) return fail(RICI_ERR_INVALID_ARGUMENT, "null out");
+    if (rici_status st = check_device()) return st;
+    if (n_needles == 0 || n_haystack == 0) return RICI_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t P = (size_t)n_bins * n_bins;
+    Staging st(s);
+    const void *dn = nullptr, *dh = nullptr;
+    void *dout = nullptr;
+    cudaError_t e = st.in(needles, sizeof(uint16_t) * P * n_needles, &dn);
+    if (e == cudaSuccess) e = st.in(haystack, sizeof(uint16_t) * P * n_haystack, &dh);
+    if (e == cudaSuccess) e = st.out(out, sizeof(uint64_t) * (size_t)n_needles * n_haystack, &dout);
+    if (e == cudaSuccess)
+        e = rici::launch_crss_search_tiles((const uint16_t *)dn, n_needles, (const uint16_t *)dh,
+                                           n_haystack, n_bins, nullptr, nullptr, (uint64_t *)dout, s);
+    if (e == cudaSuccess) e = st.finish();
+    if (e != cudaSuccess) return cuda_fail(e, "rici_crss_distances");
+    return RICI_OK;
+}
+
+rici_status rici_crss_search(const uint16_t *needles, int64_t n_needles, const uint16_t *haystack,
+                             int64_t n_haystack, int32_t n_bins, uint32_t *out_ranks,
+                             rici_stream_t stream) {
+    g_err.clear();
+    if (!valid_bins(n_bins)) return fail(RICI_ERR_INVALID_ARGUMENT, "n_bins must be in [2,128]");
+    if (rici_status st = check_images(needles, n_needles, "needles")) return st;
+    if (rici_status st = check_images(haystack, n_haystack, "haystack")) return st;
+    if (n_haystack < n_needles)
+        return fail(RICI_ERR_INVALID_ARGUMENT, "n_haystack (%lld) < n_needles (%lld): needle i "
+                    "corresponds to haystack i", (long long)n_haystack, (long long)n_needles);
+    if (n_needles > 0 && !out_ranks) return fail(RICI_ERR_INVALID_ARGUMENT, "null out_ranks");
+    if (rici_status st = check_device()) return st;
+    if (n_needles == 0) return RICI_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t P = (size_t)n_bins * n_bins;
+    Staging st(s);
+    const void *dn = nullptr, *dh = nullptr;
+    void *dr = nullptr;
+    uint64_t *thr = nullptr;
+    cudaError_t e = st.in(needles, sizeof(uint16_t) * P * n_needles, &dn);
+    if (e == cudaSuccess) e = st.in(haystack, sizeof(uint16_t) * P * n_haystack, &dh);
+    if (e == cudaSuccess) e = st.out(out_ranks, sizeof(uint32_t) * (size_t)n_needles, &dr);
+    if (e == cudaSuccess) e = cudaMallocAsync((void **)&thr, sizeof(uint64_t) * (size_t)n_needles, s);
+    if (e == cudaSuccess) {
+        st.temps.push_back(thr);
+        // a10: t_i = CRSS(n_i, h_i) ("this threshold can be trivially precomputed")
+        e = rici::launch_crss_pairs((const uint16_t *)dn, n_needles, (const uint16_t *)dh, n_haystack,
+                                    n_bins, nullptr, n_needles, thr, s);
+    }
+    if (e == cudaSuccess)
+        e = rici::launch_crss_search_tiles((const uint16_t *)dn, n_needles, (const uint16_t *)dh,
+                                           n_haystack, n_bins, thr, (uint32_t *)dr, nullptr, s);
+    if (e == cudaSuccess) e = st.finish();
+    if (e != cudaSuccess) return cuda_fail(e, "rici_crss_search");
+    return RICI_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,336 @@
+// generate.cu -- (a2-a8) RICI construction on sm_100a.
+//
+// Paper: a RICI pixel counts the intersections of a circle (radius rho_c, at
+// height beta_r on the Central Axis) with the scene surface.  It is
+// built by iterating over the triangles in three steps:
+//   1. project the triangle's vertices into the spin frame (Eqs. 1-5),
+//   2. for each layer beta in the triangle's beta-extent, intersect the layer
+//      plane with the triangle (segment E0E1), rotate it parallel to x and get
+//      the single range [min|E|, max|E|) and, when the x signs differ, the
+//      double range [|C|, min|E|) (six steps),
+//   3. increment the bins whose circle radius falls in those ranges.
+//
+// B200 design:
+//  * one CTA owns K images; their 32-bit counters live in shared memory as
+//    per-row DIFFERENCE arrays, so a segment costs <= 3 shared atomics (+2 at
+//    col(|C|), -1 at col(min), -1 at col(max)) instead of one per covered bin;
+//    a warp-shuffle prefix scan per row turns them into counts in the epilogue;
+//  * triangles stream from the chunked mesh buffer (mesh.cu); each chunk's
+//    bounding sphere is tested against the CTA's union of support spheres and
+//    chunks that cannot touch any image are skipped (exact: they add 0);
+//  * the per-image rotation coefficients are computed once per image in the
+//    CTA prologue ("out of the inner loop");
+//  * saturation to uint16 (G9) and coalesced 128-bit stores in the epilogue.
+#include "rici_internal.cuh"
+
+namespace rici {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kMaxK = 8;
+constexpr int kListCap = 4 * kThreads;   // chunk survivors per batch
+
+struct __align__(16) Frame {
+    float sx, sy, sz, valid;      // S_v (Eq. 2); valid = 0 for a zero / non-finite normal (G3)
+    float nax, nay, nbx, nbz;     // Eq. 1 with the G1 correction
+    float czx, czy, czz, pad;     // T_z = nbx*(nax x + nay y) + nbz z, Eqs. 3-4 composed
+};
+
+__device__ __forceinline__ Frame make_frame(const float *o) {
+    Frame f;
+    f.sx = o[0]; f.sy = o[1]; f.sz = o[2];
+    float nx = o[3], ny = o[4], nz = o[5];
+    float l2 = nx * nx + ny * ny + nz * nz;
+    bool ok = (l2 > 0.f) && isfinite(l2) && isfinite(f.sx) && isfinite(f.sy) && isfinite(f.sz);
+    f.valid = ok ? 1.f : 0.f;
+    f.pad = 0.f;
+    if (!ok) {
+        f.nax = 1.f; f.nay = 0.f; f.nbx = 0.f; f.nbz = 1.f; f.czx = f.czy = 0.f; f.czz = 1.f;
+        return f;
+    }
+    float l = sqrtf(l2);
+    nx /= l; ny /= l; nz /= l;                       // G3: normalise S_n
+    float la2 = nx * nx + ny * ny;
+    if (la2 > 0.f) {                                 // Eq. 1: N_a = Normalize[S_nx, S_ny]
+        float la = sqrtf(la2);
+        f.nax = nx / la; f.nay = ny / la;
+    } else {                                         // identity rotation (G2)
+        f.nax = 1.f; f.nay = 0.f;
+    }
+    float s = f.nax * nx + f.nay * ny;               // normal's x after rotation 1 (G1)
+    float lb = sqrtf(s * s + nz * nz);
+    f.nbx = s / lb; f.nbz = nz / lb;                 // N_b = Normalize[s, S_nz]
+    f.czx = f.nbx * f.nax; f.czy = f.nbx * f.nay; f.czz = f.nbz;
+    return f;
+}
+
+// First index i in [0, n] with (i + 1/2) * delta + off >= v, i.e. ceil(v/delta - off/delta - 1/2).
+// Used for rows (off = -R/2: beta_r >= v) and columns (off = 0: rho_c >= v).  Exact ties are
+// fragile pixels; the row loop re-checks membership with explicit comparisons.
+__device__ __forceinline__ int first_at_or_above(float v, float inv_delta, float off_scaled, int n) {
+    float x = fmaf(v, inv_delta, off_scaled);        // v/delta - off/delta - 1/2
+    x = fminf(fmaxf(x, -1.0f), (float)n + 1.0f);
+    int i = (int)ceilf(x);
+    return min(max(i, 0), n);
+}
+
+__device__ __forceinline__ void sort3(float &ax, float &ay, float &az, float &bx, float &by,
+                                      float &bz, float &cx, float &cy, float &cz) {
+#define RICI_SWAP(p, q) { float t = p; p = q; q = t; }
+    if (bz < az) { RICI_SWAP(ax, bx) RICI_SWAP(ay, by) RICI_SWAP(az, bz) }
+    if (cz < bz) { RICI_SWAP(bx, cx) RICI_SWAP(by, cy) RICI_SWAP(bz, cz) }
+    if (bz < az) { RICI_SWAP(ax, bx) RICI_SWAP(ay, by) RICI_SWAP(az, bz) }
+#undef RICI_SWAP
+}
+
+struct Geometry {
+    float delta, inv_delta, half_r;
+    float row_off;     // (R/2)/delta - 1/2 : row index = ceil(beta*inv_delta + row_off)
+    int n;
+};
+
+// Steps 1-6 for every layer of one projected, z-sorted triangle, accumulated
+// into the image's per-row difference arrays.
+__device__ __forceinline__ void rasterise_triangle(int *__restrict__ acc, const Geometry &g,
+                                                   float ax, float ay, float az, float bx,
+                                                   float by, float bz, float cx, float cy,
+                                                   float cz) {
+    const int N = g.n;
+    int r_lo = first_at_or_above(az, g.inv_delta, g.row_off, N);
+    int r_hi = first_at_or_above(cz, g.inv_delta, g.row_off, N);
+    for (int r = r_lo; r < r_hi; ++r) {
+        float beta = fmaf((float)r + 0.5f, g.delta, -g.half_r);
+        if (!(az <= beta && beta < cz)) continue;        // layer membership, half-open (G5)
+        // Step 1: E0 on the long edge (a,c), E1 on (a,b) below / (b,c) above the middle vertex.
+        float t = (beta - az) / (cz - az);
+        float e0x = fmaf(t, cx - ax, ax), e0y = fmaf(t, cy - ay, ay);
+        float e1x, e1y;
+        if (beta < bz) {
+            float u = (beta - az) / (bz - az);
+            e1x = fmaf(u, bx - ax, ax); e1y = fmaf(u, by - ay, ay);
+        } else {
+            float u = (beta - bz) / (cz - bz);
+            e1x = fmaf(u, cx - bx, bx); e1y = fmaf(u, cy - by, by);
+        }
+        // Step 2: rotate so E0E1 is parallel to x; the normalised direction is (cos, sin).
+        float dx = e1x - e0x, dy = e1y - e0y;
+        float l2 = dx * dx + dy * dy;
+        if (l2 == 0.f) continue;                          // zero-length slice (G5)
+        float len = sqrtf(l2);
+        float cs = dx / len, sn = dy / len;
+        float x0 = cs * e0x + sn * e0y;
+        float y = -sn * e0x + cs * e0y;
+        float x1 = x0 + len;                              // consistent with the sign test
+        // Steps 3-4: distances of E0, E1 from the axis; single range [min, max).
+        float r0 = sqrtf(e0x * e0x + e0y * e0y), r1 = sqrtf(e1x * e1x + e1y * e1y);
+        int c_min = first_at_or_above(fminf(r0, r1), g.inv_delta, -0.5f, N);
+        int c_max = first_at_or_above(fmaxf(r0, r1), g.inv_delta, -0.5f, N);
+        int *row = acc + r * N;
+        // Steps 5-6: double range [|C|, min) iff the x signs differ (x = 0 non-negative).
+        if (x0 < 0.f && x1 >= 0.f) {
+            int c_c = min(first_at_or_above(fabsf(y), g.inv_delta, -0.5f, N), c_min);
+            if (c_c == c_max) continue;
+            if (c_c < N) atomicAdd(row + c_c, 2);
+            if (c_min < N) atomicAdd(row + c_min, -1);
+            if (c_max < N) atomicAdd(row + c_max, -1);
+        } else {
+            if (c_min == c_max) continue;
+            atomicAdd(row + c_min, 1);                    // c_min < c_max <= N
+            if (c_max < N) atomicAdd(row + c_max, -1);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kThreads)
+generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere, int64_t n_chunks,
+                const float *__restrict__ origins, int64_t n, float R, int N, int K,
+                uint16_t *__restrict__ out) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ Frame frames[kMaxK];
+    __shared__ int list[kListCap];
+    __shared__ int list_n;
+    __shared__ float cta_sphere[4];
+
+    int *acc = reinterpret_cast<int *>(smem_raw);        // [K][N][N] difference arrays
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t img0 = (int64_t)blockIdx.x * K;
+    const int k_valid = (int)min((int64_t)K, n - img0);
+
+    for (int i = tid; i < K * N * N; i += kThreads) acc[i] = 0;
+    if (tid < K) {
+        if (tid < k_valid) frames[tid] = make_frame(origins + 6 * (img0 + tid));
+        else { Frame f = {}; frames[tid] = f; }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        // union of the images' support spheres (cylinder r <= R, |beta| <= R/2 -> radius R*sqrt(5)/2)
+        float lo[3] = {3e38f, 3e38f, 3e38f}, hi[3] = {-3e38f, -3e38f, -3e38f};
+        int nv = 0;
+        for (int k = 0; k < k_valid; ++k) {
+            if (frames[k].valid == 0.f) continue;
+            ++nv;
+            float p[3] = {frames[k].sx, frames[k].sy, frames[k].sz};
+            for (int a = 0; a < 3; ++a) { lo[a] = fminf(lo[a], p[a]); hi[a] = fmaxf(hi[a], p[a]); }
+        }
+        if (nv == 0) { cta_sphere[3] = -1.f; }
+        else {
+            float c[3] = {0.5f * (lo[0] + hi[0]), 0.5f * (lo[1] + hi[1]), 0.5f * (lo[2] + hi[2])};
+            float r2 = 0.f;
+            for (int k = 0; k < k_valid; ++k) {
+                if (frames[k].valid == 0.f) continue;
+                float dx = frames[k].sx - c[0], dy = frames[k].sy - c[1], dz = frames[k].sz - c[2];
+                r2 = fmaxf(r2, dx * dx + dy * dy + dz * dz);
+            }
+            float scale = fmaxf(fabsf(c[0]), fmaxf(fabsf(c[1]), fabsf(c[2])));
+            cta_sphere[0] = c[0]; cta_sphere[1] = c[1]; cta_sphere[2] = c[2];
+            cta_sphere[3] = (sqrtf(r2) + R * 1.1180340f) * (1.0f + 1e-5f) + 1e-5f * scale + 1e-30f;
+        }
+    }
+    __syncthreads();
+
+    Geometry g;
+    g.n = N;
+    g.delta = R / (float)N;
+    g.inv_delta = (float)N / R;
+    g.half_r = 0.5f * R;
+    g.row_off = 0.5f * (float)N - 0.5f;
+    const float cs_r = cta_sphere[3];
+
+    if (cs_r >= 0.f) {
+        const float ccx = cta_sphere[0], ccy = cta_sphere[1], ccz = cta_sphere[2];
+        for (int64_t base = 0; base < n_chunks; base += kListCap) {
+            if (tid == 0) list_n = 0;
+            __syncthreads();
+            for (int q = 0; q < kListCap / kThreads; ++q) {
+                int64_t c = base + q * kThreads + tid;
+                bool keep = false;
+                if (c < n_chunks) {
+                    float4 s = sphere[c];
+                    float dx = s.x - ccx, dy = s.y - ccy, dz = s.z - ccz;
+                    float rr = s.w + cs_r;
+                    keep = dx * dx + dy * dy + dz * dz <= rr * rr;
+                }
+                unsigned m = __ballot_sync(0xffffffffu, keep);
+                int pos = 0;
+                if (lane == 0 && m) pos = atomicAdd(&list_n, __popc(m));
+                pos = __shfl_sync(0xffffffffu, pos, 0);
+                if (keep) list[pos + __popc(m & ((1u << lane) - 1u))] = (int)(c - base);
+            }
+            __syncthreads();
+            const int cnt = list_n;
+            for (int e = warp; e < cnt; e += kThreads / 32) {
+                const int64_t chunk = base + list[e];
+                const float *src = tri + chunk * 9 * kChunk + lane;
+                float v[9];
+#pragma unroll
+                for (int k = 0; k < 9; ++k) v[k] = __ldg(src + k * kChunk);
+                for (int k = 0; k < k_valid; ++k) {
+                    const Frame f = frames[k];
+                    if (f.valid == 0.f) continue;
+                    // Eq. 2 (translate) then T_z of Eqs. 3-4 for the beta-extent test
+                    float p[9];
+#pragma unroll
+                    for (int j = 0; j < 3; ++j) {
+                        p[3 * j] = v[3 * j] - f.sx;
+                        p[3 * j + 1] = v[3 * j + 1] - f.sy;
+                        p[3 * j + 2] = v[3 * j + 2] - f.sz;
+                    }
+                    float z0 = fmaf(f.czx, p[0], fmaf(f.czy, p[1], f.czz * p[2]));
+                    float z1 = fmaf(f.czx, p[3], fmaf(f.czy, p[4], f.czz * p[5]));
+                    float z2 = fmaf(f.czx, p[6], fmaf(f.czy, p[7], f.czz * p[8]));
+                    float zlo = fminf(z0, fminf(z1, z2)), zhi = fmaxf(z0, fmaxf(z1, z2));
+                    int r_lo = first_at_or_above(zlo, g.inv_delta, g.row_off, N);
+                    int r_hi = first_at_or_above(zhi, g.inv_delta, g.row_off, N);
+                    if (r_lo >= r_hi) continue;
+                    // Eqs. 3-4 for T_x, T_y (alpha plane)
+                    float x[3], y[3];
+#pragma unroll
+                    for (int j = 0; j < 3; ++j) {
+                        float qx = fmaf(f.nax, p[3 * j], f.nay * p[3 * j + 1]);
+                        y[j] = fmaf(-f.nay, p[3 * j], f.nax * p[3 * j + 1]);
+                        x[j] = fmaf(f.nbz, qx, -f.nbx * p[3 * j + 2]);
+                    }
+                    float ax = x[0], ay = y[0], az = z0, bx = x[1], by = y[1], bz = z1,
+                          cx = x[2], cy = y[2], cz = z2;
+                    sort3(ax, ay, az, bx, by, bz, cx, cy, cz);
+                    rasterise_triangle(acc + k * N * N, g, ax, ay, az, bx, by, bz, cx, cy, cz);
+                }
+            }
+            __syncthreads();
+        }
+    }
+
+    // Epilogue 1: per-row inclusive prefix sum of the difference arrays (warp per row).
+    const int cpl = (N + 31) / 32;                 // columns per lane
+    for (int row = warp; row < k_valid * N; row += kThreads / 32) {
+        int *rp = acc + row * N;
+        unsigned vals[4];
+        unsigned local = 0;
+        for (int j = 0; j < cpl; ++j) {
+            int c = lane * cpl + j;
+            unsigned x = (c < N) ? (unsigned)rp[c] : 0u;
+            local += x;
+            vals[j] = local;
+        }
+        unsigned incl = local;
+        for (int o = 1; o < 32; o <<= 1) {
+            unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        unsigned excl = incl - local;
+        for (int j = 0; j < cpl; ++j) {
+            int c = lane * cpl + j;
+            if (c < N) rp[c] = (int)(vals[j] + excl);
+        }
+    }
+    __syncthreads();
+
+    // Epilogue 2: saturate to uint16 (G9) and store; 128-bit stores when aligned.
+    const int npix = N * N;
+    const int64_t total = (int64_t)k_valid * npix;
+    uint16_t *dst = out + img0 * npix;
+    const unsigned *cnt = reinterpret_cast<const unsigned *>(acc);
+    if ((npix % 8) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+        for (int64_t i = (int64_t)tid * 8; i < total; i += kThreads * 8) {
+            uint4 a = *reinterpret_cast<const uint4 *>(cnt + i);
+            uint4 b = *reinterpret_cast<const uint4 *>(cnt + i + 4);
+            uint4 o;
+            o.x = min(a.x, 65535u) | (min(a.y, 65535u) << 16);
+            o.y = min(a.z, 65535u) | (min(a.w, 65535u) << 16);
+            o.z = min(b.x, 65535u) | (min(b.y, 65535u) << 16);
+            o.w = min(b.z, 65535u) | (min(b.w, 65535u) << 16);
+            *reinterpret_cast<uint4 *>(dst + i) = o;
+        }
+    } else {
+        for (int64_t i = tid; i < total; i += kThreads) dst[i] = (uint16_t)min(cnt[i], 65535u);
+    }
+}
+
+}  // namespace
+
+int generate_images_per_cta(int N) {
+    int per = N * N * 4;
+    int k = (64 * 1024) / per;
+    return k < 1 ? 1 : (k > kMaxK ? kMaxK : k);
+}
+
+cudaError_t launch_generate(const DeviceMesh &m, const float *d_origins, int64_t n, float R, int N,
+                            uint16_t *d_out, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const int K = generate_images_per_cta(N);
+    size_t smem = (size_t)K * N * N * sizeof(int);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(generate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             200 * 1024);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    int64_t blocks = (n + K - 1) / K;
+    generate_kernel<<<(unsigned)blocks, kThreads, smem, s>>>(m.tri, m.sphere, m.n_chunks, d_origins,
+                                                             n, R, N, K, d_out);
+    note_launches(1);
+    return cudaGetLastError();
+}
+
+}  // namespace rici

@@ -1,0 +1,79 @@
+// mesh.cu -- (a1) mesh staging for the construction kernel.
+//
+// "iterate over each triangle in the scene": the construction kernel
+// streams every triangle once per group of images, so the indexed mesh
+// (vertices + index triples, D1) is de-indexed once into a device buffer laid
+// out for that stream: chunks of 32 triangles, structure-of-arrays inside a
+// chunk so one warp reads a chunk with nine coalesced 128-byte loads, plus a
+// bounding sphere per chunk that lets a CTA skip chunks that cannot reach any
+// of its images' support cylinders (an exact cull: such triangles add 0).
+#include "rici_internal.cuh"
+
+namespace rici {
+namespace {
+
+__global__ void __launch_bounds__(256)
+mesh_stage_kernel(const float *__restrict__ vertices, int64_t nv,
+                  const int32_t *__restrict__ indices, int64_t nt,
+                  float *__restrict__ tri, float4 *__restrict__ sphere,
+                  int64_t n_chunks, int *__restrict__ bad) {
+    const int lane = threadIdx.x & 31;
+    const int64_t chunk = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (chunk >= n_chunks) return;
+    int64_t t = chunk * kChunk + lane;
+    const bool real = t < nt;
+    if (!real) t = chunk * kChunk;            // pad with a copy of lane 0's vertex 0 (degenerate)
+    float v[9];
+    bool ok = true;
+    for (int j = 0; j < 3; ++j) {
+        int32_t id = indices[3 * t + (real ? j : 0)];
+        if (id < 0 || (int64_t)id >= nv) { ok = false; id = 0; }
+        v[3 * j + 0] = vertices[3 * (int64_t)id + 0];
+        v[3 * j + 1] = vertices[3 * (int64_t)id + 1];
+        v[3 * j + 2] = vertices[3 * (int64_t)id + 2];
+    }
+    if (!ok) atomicExch(bad, 1);
+    float *dst = tri + chunk * 9 * kChunk;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) dst[k * kChunk + lane] = v[k];
+
+    // chunk bounding sphere: bbox centre, max vertex distance
+    float lo[3], hi[3];
+    for (int a = 0; a < 3; ++a) {
+        lo[a] = fminf(v[a], fminf(v[3 + a], v[6 + a]));
+        hi[a] = fmaxf(v[a], fmaxf(v[3 + a], v[6 + a]));
+        for (int o = 16; o > 0; o >>= 1) {
+            lo[a] = fminf(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+            hi[a] = fmaxf(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+        }
+    }
+    float c[3] = {0.5f * (lo[0] + hi[0]), 0.5f * (lo[1] + hi[1]), 0.5f * (lo[2] + hi[2])};
+    float r2 = 0.f;
+    for (int j = 0; j < 3; ++j) {
+        float dx = v[3 * j] - c[0], dy = v[3 * j + 1] - c[1], dz = v[3 * j + 2] - c[2];
+        r2 = fmaxf(r2, dx * dx + dy * dy + dz * dz);
+    }
+    for (int o = 16; o > 0; o >>= 1) r2 = fmaxf(r2, __shfl_xor_sync(0xffffffffu, r2, o));
+    if (lane == 0) {
+        float scale = fmaxf(fabsf(c[0]), fmaxf(fabsf(c[1]), fabsf(c[2])));
+        float r = sqrtf(r2) * (1.0f + 1e-5f) + 1e-6f * scale + 1e-30f;   // conservative pad
+        sphere[chunk] = make_float4(c[0], c[1], c[2], r);
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_mesh_stage(const float *d_vertices, int64_t nv, const int32_t *d_indices,
+                              int64_t nt, DeviceMesh *m, int *d_bad, cudaStream_t s) {
+    m->nt = nt;
+    m->n_chunks = (nt + kChunk - 1) / kChunk;
+    if (m->n_chunks == 0) return cudaSuccess;
+    const int warps = 8;
+    int64_t blocks = (m->n_chunks + warps - 1) / warps;
+    mesh_stage_kernel<<<(unsigned)blocks, 32 * warps, 0, s>>>(d_vertices, nv, d_indices, nt, m->tri,
+                                                             m->sphere, m->n_chunks, d_bad);
+    note_launches(1);
+    return cudaGetLastError();
+}
+
+}  // namespace rici

@@ -1,0 +1,44 @@
+// rici_internal.cuh -- internal declarations shared by the CUDA translation units
+// of librici.so (product path; never includes or links anything from oracle/).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rici {
+
+// Triangles are stored in chunks of kChunk, structure-of-arrays inside a chunk:
+// tri[(chunk*9 + k)*kChunk + lane], k = 0..8 -> v0.x v0.y v0.z v1.x ... v2.z.
+// A warp loads one chunk with 9 fully coalesced 128-byte loads.
+constexpr int kChunk = 32;
+
+struct DeviceMesh {
+    int64_t nt = 0;          // triangles
+    int64_t n_chunks = 0;    // ceil(nt / kChunk)
+    float *tri = nullptr;    // [n_chunks][9][kChunk]
+    float4 *sphere = nullptr;// [n_chunks] bounding sphere (cx, cy, cz, r) of each chunk
+    int device = 0;
+};
+
+// Kernel-launch bookkeeping (rici_launch_count()).
+void note_launches(int k);
+
+// a1: de-index + chunk layout + chunk spheres; *d_bad set to 1 on an out-of-range index.
+cudaError_t launch_mesh_stage(const float *d_vertices, int64_t nv, const int32_t *d_indices,
+                              int64_t nt, DeviceMesh *m, int *d_bad, cudaStream_t s);
+
+// a2-a8: RICI construction.
+cudaError_t launch_generate(const DeviceMesh &m, const float *d_origins, int64_t n, float R,
+                            int N, uint16_t *d_out, cudaStream_t s);
+
+// a10: out[k] = CRSS(needles[pairs[k].x], haystack[pairs[k].y]); pairs = nullptr -> (k,k).
+cudaError_t launch_crss_pairs(const uint16_t *d_needles, int64_t nn, const uint16_t *d_haystack,
+                              int64_t nh, int N, const int64_t *d_pairs, int64_t m,
+                              uint64_t *d_out, cudaStream_t s);
+
+// a9 + a11 + a12: count (thresholds != nullptr) or full distances (d_dist != nullptr).
+cudaError_t launch_crss_search_tiles(const uint16_t *d_needles, int64_t nn,
+                                     const uint16_t *d_haystack, int64_t nh, int N,
+                                     const uint64_t *d_thresholds, uint32_t *d_counts,
+                                     uint64_t *d_dist, cudaStream_t s);
+
+}  // namespace rici

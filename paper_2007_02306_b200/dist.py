@@ -1,0 +1,84 @@
+"""Data-parallel sharding of the RICI hot path over the GPUs of one node.
+
+Construction (a2-a8): the oriented points are split into contiguous blocks, one per rank;
+the mesh is replicated; no collective -- each rank's image block IS its haystack shard.
+
+Search (a9-a12): the haystack is split into contiguous blocks; the needle set is on
+every rank (broadcast once); the only exchange steps are
+  * thresholds t_i = CRSS(n_i, h_i): computed by the rank that owns h_i (a10), combined
+    with all_reduce(MAX) (non-owners contribute 0), and
+  * ranks: each rank counts haystack images closer than t_i in its shard (a11 + a12),
+    then all_reduce(SUM) of the per-needle partial counts.
+Integer counts summed exactly, so ranks are identical for every world size.
+
+The compute calls default to the CUDA library; ``ops`` lets the CPU tests drive the same
+host logic (sharding arithmetic, collectives) under the gloo backend.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable
+
+import torch
+import torch.distributed as dist
+
+
+def shard_range(n: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous block [lo, hi) of ``n`` items for ``rank`` of ``world`` (sizes differ by <= 1)."""
+    base, extra = divmod(n, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+@dataclass
+class SearchOps:
+    """Compute primitives used by :func:`search_sharded` (defaults: librici.so)."""
+    pairs: Callable        # (needles, haystack_shard, pairs[m,2] int64) -> uint64 CRSS (int64 storage)
+    count_below: Callable  # (needles, haystack_shard, thresholds) -> per-needle counts (int32)
+
+
+def cuda_ops() -> SearchOps:
+    from . import rici_crss_count_below, rici_crss_pairs
+    return SearchOps(pairs=rici_crss_pairs, count_below=rici_crss_count_below)
+
+
+def generate_sharded(mesh, origins: torch.Tensor, support_radius: float, n_bins: int = 64,
+                     group=None, generate: Callable | None = None):
+    """Each rank generates the images of its block of ``origins`` (the full [n,6] array).
+    Returns (images of the block, (lo, hi))."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    lo, hi = shard_range(origins.shape[0], world, rank)
+    if generate is None:
+        from . import rici_generate as generate
+    return generate(mesh, origins[lo:hi].contiguous(), support_radius, n_bins), (lo, hi)
+
+
+def search_sharded(needles: torch.Tensor, haystack_shard: torch.Tensor, shard_lo: int,
+                   n_bins: int = 64, group=None, ops: SearchOps | None = None) -> torch.Tensor:
+    """Ranks of needle i's correspondence haystack i over the union of all ranks' shards.
+
+    needles         [n_needles, N, N] on every rank (uint16 in int16 storage)
+    haystack_shard  this rank's contiguous block of the global haystack, starting at global
+                    index ``shard_lo``
+    Returns int64 ranks [n_needles] on every rank.
+    """
+    ops = ops or cuda_ops()
+    nn = needles.shape[0]
+    dev = needles.device
+    n_local = haystack_shard.shape[0]
+    # a10 on the owner of h_i: needles whose correspondence lies in [shard_lo, shard_lo + n_local)
+    lo = max(0, min(shard_lo, nn))
+    hi = max(lo, min(shard_lo + n_local, nn))
+    thr = torch.zeros(nn, dtype=torch.int64, device=dev)
+    if hi > lo:
+        idx = torch.arange(lo, hi, dtype=torch.int64, device=dev)
+        pairs = torch.stack([idx, idx - shard_lo], 1).contiguous()
+        thr[lo:hi] = ops.pairs(needles, haystack_shard, pairs, n_bins)
+    if dist.is_initialized():
+        # thresholds are uint64 in int64 storage; CRSS <= 4032 * 131070^2 < 2^63, so MAX is exact
+        dist.all_reduce(thr, op=dist.ReduceOp.MAX, group=group)
+    counts = ops.count_below(needles, haystack_shard, thr, n_bins).to(torch.int64)
+    if dist.is_initialized():
+        dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
+    return counts

@@ -1,0 +1,68 @@
+"""Host-side checks of the C ABI that need no GPU: the library builds for sm_100a, loads,
+exports every symbol include/rici.h declares, validates arguments before touching a device,
+and the product package never imports the oracle."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2007_02306_b200 import build as b
+    b.build()
+    from paper_2007_02306_b200 import _lib
+    return _lib.load()
+
+
+def _declared():
+    txt = open(os.path.join(ROOT, "include", "rici.h")).read()
+    return sorted(set(re.findall(r"RICI_API[^;]*?\b(rici_\w+)\s*\(", txt, re.S)))
+
+
+def test_header_symbols_exported(lib):
+    declared = _declared()
+    assert len(declared) == 11
+    out = subprocess.run(["nm", "-D", "--defined-only", os.path.join(ROOT, "paper_2007_02306_b200", "librici.so")],
+                         capture_output=True, text=True, check=True).stdout
+    exported = set(re.findall(r" T (rici_\w+)", out))
+    assert set(declared) <= exported
+    for name in declared:
+        assert hasattr(lib, name)
+
+
+def test_sass_is_sm100a():
+    so = os.path.join(ROOT, "paper_2007_02306_b200", "librici.so")
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", so], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_version_and_argument_validation(lib):
+    assert lib.rici_version().decode().startswith("rici-b200")
+    P = ctypes.c_void_p
+    # null mesh / bad sizes are rejected synchronously, before any device work
+    assert lib.rici_generate(None, None, 0, ctypes.c_float(0.3), 64, None, None) == 1
+    h = P()
+    assert lib.rici_create_mesh(None, -1, None, 0, None, ctypes.byref(h)) == 1
+    assert b"negative" in lib.rici_last_error()
+    assert lib.rici_crss_search(None, 5, None, 5, 64, None, None) == 1
+    assert lib.rici_crss_search(P(1), 6, P(1), 5, 64, P(1), None) == 1      # n_haystack < n_needles
+    assert lib.rici_crss_pairs(P(1), 1, P(1), 1, 1, P(1), 1, P(1), None) == 1  # n_bins < 2
+    assert lib.rici_crss_distances(P(1), 1, P(1), 1, 129, P(1), None) == 1    # n_bins > 128
+    assert lib.rici_destroy_mesh(None) == 0
+    assert lib.rici_mesh_num_triangles(None) == -1
+
+
+def test_product_does_not_touch_oracle():
+    pkg = os.path.join(ROOT, "paper_2007_02306_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".c")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert not re.search(r"^\s*(import|from)\s+oracle\b", txt, re.M), f
+                assert "librici_oracle" not in txt and "rici_oracle.c" not in txt, f
+                assert not re.search(r"#include\s*[<\"].*oracle", txt), f

@@ -1,0 +1,230 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+RICI images (north star): at most 1e-4 of the pixels may differ and every differing
+pixel must be fragile -- its oracle count changes when the circle moves by up to
+tau = 1e-5*R in beta and/or rho.  Closed-form hand cases must match exactly.
+CRSS distances and ranks: bit-exact on identical images.
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def rici():
+    import paper_2007_02306_b200 as r
+    r._lib.load()
+    assert torch.cuda.is_available()
+    return r
+
+
+DEV = "cuda:0"
+
+
+def _gen(rici, mesh, origins, R, N):
+    m = rici.rici_create_mesh(torch.from_numpy(mesh.vertices).to(DEV), torch.from_numpy(mesh.indices).to(DEV))
+    o = torch.from_numpy(np.ascontiguousarray(origins, dtype=np.float32)).to(DEV)
+    out = rici.rici_generate(m, o, R, N)
+    torch.cuda.synchronize()
+    return out.cpu().numpy().view(np.uint16)
+
+
+def _assert_parity(gpu, ref):
+    diff = gpu != ref["images"]
+    n_bad = int((diff & ~ref["fragile"]).sum())
+    assert n_bad == 0, f"{n_bad} non-attributable differing pixels"
+    assert diff.mean() <= 1e-4, f"{int(diff.sum())} differing pixels ({diff.mean():.2e})"
+    return int(diff.sum())
+
+
+def test_c1_icosphere(rici, oracle_mod):
+    cfg = synth.config_c1()
+    g = _gen(rici, cfg["mesh"], cfg["origins"], cfg["R"], cfg["N"])
+    ref = oracle_mod.rici_generate(cfg["mesh"].vertices, cfg["mesh"].indices, cfg["origins"],
+                                   cfg["R"], cfg["N"], fragile=True)
+    _assert_parity(g, ref)
+
+
+def test_h2_single_triangle_small_N(rici, oracle_mod):
+    m = synth.Mesh(np.array([[1, -2, -1], [1, -2, 2], [1, 2, -1]], np.float32),
+                   np.array([[0, 1, 2]], np.int32), np.zeros((3, 3), np.float32))
+    o = np.array([[0, 0, 0, 0, 0, 1]], np.float32)
+    g = _gen(rici, m, o, 4.0, 8)
+    assert np.array_equal(g, oracle_mod.rici_generate(m.vertices, m.indices, o, 4.0, 8)["images"])
+
+
+def test_cube_and_tetra_closed_forms(rici, oracle_mod):
+    c = synth.cube()
+    corners = np.array([[x, y, z] for x in (-1, 1) for y in (-1, 1) for z in (-1, 1)], np.float32)
+    o = np.concatenate([corners, corners / np.sqrt(3)], 1).astype(np.float32)
+    g = _gen(rici, c, o, 1.0, 64)
+    assert np.array_equal(g, oracle_mod.rici_generate(c.vertices, c.indices, o, 1.0, 64)["images"])
+    assert (g.reshape(8, -1).sum(1) == 2184).all()
+    t = synth.tetrahedron()
+    s = 1 / np.sqrt(3)
+    o = np.array([[1, 1, 1, s, s, s]], np.float32)
+    g = _gen(rici, t, o, 1.0, 64)
+    assert g.sum() == 1080
+
+
+@pytest.mark.parametrize("N", [2, 8, 30, 64, 100, 128])
+def test_bin_counts(rici, oracle_mod, N):
+    m = synth.bumpy_torus(60, 30, key=(9,))
+    o = m.origins[::37]
+    g = _gen(rici, m, o, 0.3, N)
+    ref = oracle_mod.rici_generate(m.vertices, m.indices, o, 0.3, N, fragile=True)
+    _assert_parity(g, ref)
+
+
+@pytest.mark.parametrize("case", ["soup", "grid_soup", "far_scene"])
+def test_adversarial(rici, oracle_mod, case):
+    if case == "soup":
+        m = synth.triangle_soup(700, (5,), extent=0.5)
+        o, R = synth.random_origins(67, (6,), 0.3), 0.5
+    elif case == "grid_soup":
+        m = synth.triangle_soup(700, (7,), extent=0.5, grid=1 / 32)
+        o = synth.random_origins(67, (8,), 0.3)
+        o[:, :3] = np.round(o[:, :3] * 32) / 32
+        o[::3, 3:] = [0, 0, 1]
+        o[1::3, 3:] = [0, 0, -1]
+        R = 0.5
+    else:
+        # scene far from the origin: float cancellation in P - S_v (translate first, Eq. 2)
+        m = synth.bumpy_torus(80, 40, key=(13,))
+        m = synth.place(m, synth.random_rotation(np.random.default_rng(3)), [2.7, 1.3, 2.2])
+        o, R = m.origins[::13], 0.3
+    g = _gen(rici, m, o, R, 64)
+    ref = oracle_mod.rici_generate(m.vertices, m.indices, o, R, 64, fragile=True)
+    # the soups are made of large overlapping triangles (counts > 100): per-image fraction is
+    # checked against the combined pixel count of the case
+    _assert_parity(g, ref)
+
+
+def test_degenerate_inputs(rici):
+    c = synth.cube()
+    o = np.array([[1, 1, 1, 0, 0, 0], [1, 1, 1, np.nan, 0, 1], [50, 50, 50, 0, 0, 1]], np.float32)
+    g = _gen(rici, c, o, 1.0, 64)
+    assert not g.any()
+    empty = synth.Mesh(np.zeros((0, 3), np.float32), np.zeros((0, 3), np.int32), np.zeros((0, 3), np.float32))
+    g = _gen(rici, empty, synth.random_origins(5, (1,)), 1.0, 64)
+    assert g.shape == (5, 64, 64) and not g.any()
+    # zero images requested
+    m = rici.rici_create_mesh(torch.from_numpy(c.vertices).to(DEV), torch.from_numpy(c.indices).to(DEV))
+    out = rici.rici_generate(m, torch.zeros((0, 6), device=DEV), 1.0, 64)
+    assert out.shape == (0, 64, 64)
+
+
+def test_bad_index_rejected(rici):
+    v = torch.zeros((3, 3), device=DEV)
+    t = torch.tensor([[0, 1, 3]], dtype=torch.int32, device=DEV)
+    with pytest.raises(rici.RiciError) as e:
+        rici.rici_create_mesh(v, t)
+    assert e.value.status == 1
+
+
+def test_c2_sampled(rici, oracle_mod):
+    """C2 at full size (34,848 images, the bench launch configuration); oracle on a sample."""
+    cfg = synth.config_c2()
+    m = cfg["mesh"]
+    g = _gen(rici, m, cfg["origins"], cfg["R"], cfg["N"])
+    rng = np.random.default_rng(0)
+    idx = np.sort(rng.choice(m.n_vertices, 600, replace=False))
+    idx[-1] = m.n_vertices - 1                               # the ragged tail
+    ref = oracle_mod.rici_generate(m.vertices, m.indices, cfg["origins"][idx], cfg["R"], cfg["N"], fragile=True)
+    _assert_parity(g[idx], ref)
+    # property at full size: closed surface -> even counts except fragile pixels (sampled above)
+    assert (g % 2 == 1).mean() < 1e-4
+
+
+def test_host_pointer_path_equals_device_path(rici):
+    cfg = synth.config_c1()
+    m = cfg["mesh"]
+    dev = _gen(rici, m, cfg["origins"], cfg["R"], cfg["N"])
+    hm = rici.rici_create_mesh(m.vertices, m.indices)                  # numpy -> host pointers
+    host = rici.rici_generate(hm, cfg["origins"], cfg["R"], cfg["N"])
+    assert np.array_equal(host.numpy().view(np.uint16), dev)
+    r_host = rici.rici_crss_search(host, host)
+    r_dev = rici.rici_crss_search(torch.from_numpy(dev.view(np.int16)).to(DEV),
+                                  torch.from_numpy(dev.view(np.int16)).to(DEV))
+    assert np.array_equal(r_host.numpy(), r_dev.cpu().numpy())
+
+
+# ------------------------------------------------------------------------------- CRSS
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int16)).to(DEV)
+
+
+def _rand_imgs(rng, k, N=64, hi=12, density=0.3):
+    a = rng.integers(0, hi, (k, N, N))
+    a[rng.random((k, N, N)) > density] = 0
+    return a.astype(np.uint16)
+
+
+def test_crss_distances_c1_bit_exact(rici, oracle_mod):
+    cfg = synth.config_c1()
+    g = _gen(rici, cfg["mesh"], cfg["origins"], cfg["R"], cfg["N"])
+    d = rici.rici_crss_distances(_dev(g), _dev(g)).cpu().numpy().view(np.uint64)
+    assert np.array_equal(d, oracle_mod.crss_matrix(g, g))
+    assert set(np.unique(d)) <= {0, 8856, 10908}
+    r = rici.rici_crss_search(_dev(g), _dev(g)).cpu().numpy()
+    assert not r.any()
+
+
+@pytest.mark.parametrize("hi,nn,nh,N", [(12, 70, 101, 64), (300, 33, 65, 64), (70000, 5, 40, 64),
+                                         (12, 1100, 37, 64), (9, 20, 45, 16), (5, 9, 33, 128)])
+def test_crss_distances_random_bit_exact(rici, oracle_mod, hi, nn, nh, N):
+    """Spans needle chunks (1100 > 1024), ragged haystack tiles, the 64-bit path (values > 127,
+    up to uint16 saturation), small and large N."""
+    rng = np.random.default_rng(hi + nn)
+    A = _rand_imgs(rng, nn, N=N, hi=min(hi, 65536), density=0.3)
+    B = _rand_imgs(rng, nh, N=N, hi=min(hi, 65536), density=0.5)
+    if hi > 65535:
+        A[0, :, 1::2] = 65535
+        B[1, :, 0::2] = 65535
+    d = rici.rici_crss_distances(_dev(A), _dev(B)).cpu().numpy().view(np.uint64)
+    assert np.array_equal(d, oracle_mod.crss_matrix(A, B))
+
+
+def test_crss_pairs_and_count_below(rici, oracle_mod):
+    rng = np.random.default_rng(5)
+    A = _rand_imgs(rng, 50, density=0.1)
+    B = _rand_imgs(rng, 300, density=0.4)
+    pairs = np.stack([rng.integers(0, 50, 200), rng.integers(0, 300, 200)], 1).astype(np.int64)
+    pairs[0] = [49, 299]
+    got = rici.rici_crss_pairs(_dev(A), _dev(B), torch.from_numpy(pairs).to(DEV)).cpu().numpy().view(np.uint64)
+    D = oracle_mod.crss_matrix(A, B)
+    assert np.array_equal(got, D[pairs[:, 0], pairs[:, 1]])
+    bad = torch.tensor([[0, 300]], dtype=torch.int64, device=DEV)           # device pairs: sentinel
+    assert rici.rici_crss_pairs(_dev(A), _dev(B), bad).cpu().numpy().view(np.uint64)[0] == 2**64 - 1
+    with pytest.raises(rici.RiciError):                                      # host pairs: error
+        rici.rici_crss_pairs(_dev(A), _dev(B), np.array([[0, 300]], np.int64))
+    thr = D[np.arange(50), rng.integers(0, 300, 50)]
+    cnt = rici.rici_crss_count_below(_dev(A), _dev(B), torch.from_numpy(thr.view(np.int64)).to(DEV))
+    assert np.array_equal(cnt.cpu().numpy().astype(np.uint32), oracle_mod.count_below(A, B, thr))
+
+
+def test_ranks_c2_sampled_needles_full_haystack(rici, oracle_mod):
+    """C2 self-search at full size on the GPU (the bench configuration); the oracle checks a
+    sample of needles against the full 34,848-image haystack."""
+    cfg = synth.config_c2()
+    g = _gen(rici, cfg["mesh"], cfg["origins"], cfg["R"], cfg["N"])
+    gd = _dev(g)
+    ranks = rici.rici_crss_search(gd, gd).cpu().numpy()
+    rng = np.random.default_rng(1)
+    idx = np.sort(rng.choice(g.shape[0], 24, replace=False))
+    thr = np.array([oracle_mod.crss(g[i], g[i]) for i in idx], np.uint64)
+    want = oracle_mod.count_below(g[idx], g, thr)
+    assert np.array_equal(ranks[idx].astype(np.uint32), want)
+    assert (ranks >= 0).all() and (ranks < g.shape[0]).all()
+
+
+def test_ranks_ties_and_duplicates(rici, oracle_mod):
+    rng = np.random.default_rng(7)
+    A = _rand_imgs(rng, 40, N=64, hi=3, density=0.05)
+    H = np.concatenate([A, A[::-1], _rand_imgs(rng, 29, hi=3, density=0.05)])   # duplicates -> ties
+    r = rici.rici_crss_search(_dev(A), _dev(H)).cpu().numpy()
+    assert np.array_equal(r.astype(np.uint32), oracle_mod.ranks(A, H))
