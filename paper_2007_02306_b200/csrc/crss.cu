@@ -29,8 +29,9 @@ namespace rici {
 namespace {
 
 constexpr int kTileImages = 32;          // one haystack image per lane
-constexpr int kCrssThreads = 512;
-constexpr int kNeedleChunk = 1024;
+constexpr int kCrssThreads = 1024;
+constexpr int kNeedleChunk = 2048;
+constexpr int kWarpBuf = 512;            // per-warp staged needle entries (int32)
 constexpr int kSmallMax = 127;
 constexpr int kPixBits = 14;             // pixel index bits (N <= 128)
 
@@ -94,6 +95,9 @@ needle_prepare_kernel(const uint16_t *__restrict__ needles, int64_t nn, int N, i
         if (dn != 0) dst[cnt + __popc(m & ((1u << lane) - 1u))] = dn * (1 << kPixBits) + p;
         cnt += __popc(m);
     }
+    // pad to a multiple of 4 with entry 0 = (D_n 0, pixel 0): column 0 has D_h = 0 in the
+    // staged planes, so a pad entry adds (0 - 0)^2 = 0
+    if (lane < ((4 - (cnt & 3)) & 3)) dst[cnt + lane] = 0;
     for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (lane == 0) { n_entries[i] = cnt; small[i] = mx <= (unsigned)kSmallMax; }
 }
@@ -109,17 +113,40 @@ struct TileArgs {
     unsigned long long *work;
 };
 
+__device__ __forceinline__ unsigned pack4(int a, int b, int c, int d) {
+    return (unsigned)(a & 0xff) | ((unsigned)(b & 0xff) << 8) | ((unsigned)(c & 0xff) << 16) |
+           ((unsigned)d << 24);
+}
+
+// One masked Eq. 7 term for this lane's haystack image: (D_n - D_h)^2.  Planes have a
+// power-of-two stride S and are XOR-swizzled at 4-byte granularity by the image index, so
+// the shared address of pixel p in lane j's plane is (p & (S-1)) ^ key_j with
+// key_j = (tile_base + j*S) | (j << 2): one LOP3, and the 32 lanes hit 32 distinct banks.
+__device__ __forceinline__ int sq_term(int entry, unsigned mask, unsigned key) {
+    int dh;
+    asm volatile("ld.shared.s8 %0, [%1];" : "=r"(dh) : "r"(((unsigned)entry & mask) ^ key));
+    int d = (entry >> kPixBits) - dh;
+    return d * d;
+}
+
 __global__ void __launch_bounds__(kCrssThreads, 1)
 crss_tile_kernel(TileArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    signed char *dh = reinterpret_cast<signed char *>(smem_raw);   // [32][plane_bytes]
+    // [32][S] int8 planes, S = A.plane_bytes (power of two), aligned to S in the shared window
+    const unsigned S = (unsigned)A.plane_bytes;
+    const unsigned raw_sh = (unsigned)__cvta_generic_to_shared(smem_raw);
+    const unsigned pad = S ? ((S - (raw_sh & (S - 1))) & (S - 1)) : 0u;
+    unsigned char *dh = smem_raw + pad;
+    const unsigned tile_sh = raw_sh + pad;
+    int *wbuf_all = reinterpret_cast<int *>(smem_raw + (S ? S : 16) + kTileImages * S);  // [warps][kWarpBuf]
     __shared__ unsigned cnt_s[kNeedleChunk];
     __shared__ long long item_s;
-    __shared__ int tile_small_s;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nwarps = kCrssThreads / 32;
     const int N = A.N, P = N * N;
+    int *wbuf = wbuf_all + warp * kWarpBuf;
+    const bool vec_stage = (N % 8) == 0;
 
     for (;;) {
         __syncthreads();
@@ -138,28 +165,57 @@ crss_tile_kernel(TileArgs A) {
             const int64_t j0 = tile * kTileImages;
             const int nj = (int)min((int64_t)kTileImages, A.nh - j0);
             __syncthreads();                              // previous tile fully consumed
-            // stage D_h(r,c) = h[r][c] - h[r][c-1] as int8 planes (0 in column 0)
+            // stage D_h(r,c) = h[r][c] - h[r][c-1] as int8 planes (0 in column 0); the left
+            // neighbour of a thread's 8-pixel run comes from the previous lane
             int small_local = 1;
             if (A.use_smem) {
-                for (int q = tid; q < kTileImages * P; q += kCrssThreads) {
-                    int j = q / P, p = q - j * P;
-                    int v = 0;
-                    if (j < nj) {
-                        const uint16_t *h = A.hay + (j0 + j) * (int64_t)P;
-                        int x = __ldg(h + p);
-                        int xl = (p % N) ? (int)__ldg(h + p - 1) : x;
-                        small_local &= (x <= kSmallMax);
-                        v = x - xl;
+                if (vec_stage) {
+                    const int runs = P / 8;               // per image
+                    for (int q0 = 0; q0 < kTileImages * runs; q0 += kCrssThreads) {
+                        const int q = q0 + tid;
+                        const int j = q / runs, p = (q - j * runs) * 8;
+                        uint4 w = make_uint4(0, 0, 0, 0);
+                        const bool live = (q < kTileImages * runs) && j < nj;
+                        if (live) w = __ldg(reinterpret_cast<const uint4 *>(A.hay + (j0 + j) * (int64_t)P + p));
+                        unsigned prev_hi = __shfl_up_sync(0xffffffffu, w.w, 1);
+                        int left;
+                        if (p % N == 0) left = (int)(w.x & 0xffff);          // column 0: D_h = 0
+                        else if (lane == 0) left = live ? (int)__ldg(A.hay + (j0 + j) * (int64_t)P + p - 1) : 0;
+                        else left = (int)(prev_hi >> 16);
+                        int x[8] = {(int)(w.x & 0xffff), (int)(w.x >> 16), (int)(w.y & 0xffff), (int)(w.y >> 16),
+                                    (int)(w.z & 0xffff), (int)(w.z >> 16), (int)(w.w & 0xffff), (int)(w.w >> 16)};
+                        int mx = max(max(max(x[0], x[1]), max(x[2], x[3])), max(max(x[4], x[5]), max(x[6], x[7])));
+                        small_local &= (mx <= kSmallMax);
+                        if (q < kTileImages * runs) {
+                            unsigned char *pl = dh + j * S;
+                            const unsigned key = (unsigned)j << 2;
+                            *reinterpret_cast<unsigned *>(pl + ((unsigned)p ^ key)) =
+                                pack4(x[0] - left, x[1] - x[0], x[2] - x[1], x[3] - x[2]);
+                            *reinterpret_cast<unsigned *>(pl + ((unsigned)(p + 4) ^ key)) =
+                                pack4(x[4] - x[3], x[5] - x[4], x[6] - x[5], x[7] - x[6]);
+                        }
                     }
-                    dh[j * A.plane_bytes + p] = (signed char)v;
+                } else {
+                    for (int q = tid; q < kTileImages * P; q += kCrssThreads) {
+                        int j = q / P, p = q - j * P;
+                        int v = 0;
+                        if (j < nj) {
+                            const uint16_t *h = A.hay + (j0 + j) * (int64_t)P;
+                            int x = __ldg(h + p);
+                            int xl = (p % N) ? (int)__ldg(h + p - 1) : x;
+                            small_local &= (x <= kSmallMax);
+                            v = x - xl;
+                        }
+                        dh[j * S + ((unsigned)p ^ ((unsigned)j << 2))] = (unsigned char)(signed char)v;
+                    }
                 }
             } else {
                 small_local = 0;
             }
-            int tile_small = __syncthreads_and(small_local);
-            (void)tile_small_s;
+            const int tile_small = __syncthreads_and(small_local);
 
-            const signed char *mine = dh + lane * A.plane_bytes;
+            const unsigned mask = S - 1u;
+            const unsigned key = (tile_sh + (unsigned)lane * S) | ((unsigned)lane << 2);
             const bool valid = lane < nj;
             const int64_t gj = j0 + lane;
             for (int il = warp; il < nc; il += nwarps) {
@@ -168,20 +224,26 @@ crss_tile_kernel(TileArgs A) {
                 const int *L = A.entries + gi * (int64_t)A.cap;
                 uint64_t d;
                 if (tile_small && A.small[gi]) {
+                    // fast path: |D_n|,|D_h| <= 127 -> every term <= 254^2, sum < 2^32
+                    const int ne4 = (ne + 3) & ~3;
                     unsigned acc = 0;
-                    int e = 0;
-                    for (; e + 4 <= ne; e += 4) {
-                        int v0 = __ldg(L + e), v1 = __ldg(L + e + 1), v2 = __ldg(L + e + 2), v3 = __ldg(L + e + 3);
-                        int d0 = (v0 >> kPixBits) - mine[v0 & ((1 << kPixBits) - 1)];
-                        int d1 = (v1 >> kPixBits) - mine[v1 & ((1 << kPixBits) - 1)];
-                        int d2 = (v2 >> kPixBits) - mine[v2 & ((1 << kPixBits) - 1)];
-                        int d3 = (v3 >> kPixBits) - mine[v3 & ((1 << kPixBits) - 1)];
-                        acc += (unsigned)(d0 * d0) + (unsigned)(d1 * d1) + (unsigned)(d2 * d2) + (unsigned)(d3 * d3);
-                    }
-                    for (; e < ne; ++e) {
-                        int v0 = __ldg(L + e);
-                        int d0 = (v0 >> kPixBits) - mine[v0 & ((1 << kPixBits) - 1)];
-                        acc += (unsigned)(d0 * d0);
+                    for (int s0 = 0; s0 < ne4; s0 += kWarpBuf) {
+                        const int sn = min(kWarpBuf, ne4 - s0);
+                        __syncwarp();
+                        for (int e = lane * 4; e < sn; e += 128)
+                            *reinterpret_cast<int4 *>(wbuf + e) = __ldg(reinterpret_cast<const int4 *>(L + s0 + e));
+                        __syncwarp();
+                        int e = 0;
+                        for (; e + 8 <= sn; e += 8) {
+                            const int4 u = *reinterpret_cast<const int4 *>(wbuf + e);
+                            const int4 v = *reinterpret_cast<const int4 *>(wbuf + e + 4);
+                            acc += (unsigned)(sq_term(u.x, mask, key) + sq_term(u.y, mask, key) + sq_term(u.z, mask, key) + sq_term(u.w, mask, key));
+                            acc += (unsigned)(sq_term(v.x, mask, key) + sq_term(v.y, mask, key) + sq_term(v.z, mask, key) + sq_term(v.w, mask, key));
+                        }
+                        if (e < sn) {
+                            const int4 u = *reinterpret_cast<const int4 *>(wbuf + e);
+                            acc += (unsigned)(sq_term(u.x, mask, key) + sq_term(u.y, mask, key) + sq_term(u.z, mask, key) + sq_term(u.w, mask, key));
+                        }
                     }
                     d = acc;
                 } else {
@@ -240,7 +302,7 @@ cudaError_t launch_crss_search_tiles(const uint16_t *d_needles, int64_t nn,
     }
     if (nn == 0 || nh == 0) return cudaSuccess;
     const int P = N * N;
-    const int cap = N * (N - 1) > 0 ? N * (N - 1) : 1;
+    const int cap = ((N * (N - 1) + 3) / 4) * 4;        // int4-aligned list stride
     int *entries = nullptr, *n_entries = nullptr;
     unsigned char *small = nullptr;
     unsigned long long *work = nullptr;
@@ -265,12 +327,13 @@ cudaError_t launch_crss_search_tiles(const uint16_t *d_needles, int64_t nn,
     A.entries = entries; A.n_entries = n_entries; A.small = small; A.cap = cap;
     A.thr = d_thresholds; A.counts = d_counts; A.dist = d_dist;
     A.N = N;
-    int words = (P + 3) / 4;
-    if ((words & 1) == 0) words += 1;                    // odd word stride: lanes hit distinct banks
-    A.plane_bytes = 4 * words;
-    size_t smem = (size_t)kTileImages * A.plane_bytes;
-    A.use_smem = smem <= 200 * 1024;
-    if (!A.use_smem) smem = 16;
+    int stride = 128;                                    // power of two >= P (XOR swizzle needs >= 128)
+    while (stride < P) stride <<= 1;
+    A.plane_bytes = stride;
+    size_t smem = (size_t)(kTileImages + 1) * stride;    // + alignment slack
+    A.use_smem = (kTileImages * (size_t)stride <= 128 * 1024) && P < (1 << kPixBits);
+    if (!A.use_smem) { smem = 16; A.plane_bytes = 0; }
+    smem += (size_t)(kCrssThreads / 32) * kWarpBuf * sizeof(int);
     A.n_tiles = (nh + kTileImages - 1) / kTileImages;
     int64_t n_chunks = (nn + kNeedleChunk - 1) / kNeedleChunk;
     int dev = 0, sms = 148;
@@ -284,11 +347,11 @@ cudaError_t launch_crss_search_tiles(const uint16_t *d_needles, int64_t nn,
     A.n_groups = (A.n_tiles + A.tiles_per_group - 1) / A.tiles_per_group;
     A.n_items = n_chunks * A.n_groups;
     A.work = work;
-    static bool attr_set = false;
-    if (!attr_set) {
-        e = cudaFuncSetAttribute(crss_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+    static size_t attr_smem = 0;                          // static + dynamic must stay <= 227 KB
+    if (smem > attr_smem) {
+        e = cudaFuncSetAttribute(crss_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        attr_set = true;
+        attr_smem = smem;
     }
     int64_t grid = A.n_items < sms ? A.n_items : sms;
     crss_tile_kernel<<<(unsigned)grid, kCrssThreads, smem, s>>>(A);

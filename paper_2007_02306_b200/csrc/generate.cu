@@ -141,6 +141,26 @@ __device__ __forceinline__ void rasterise_triangle(int *__restrict__ acc, const 
     }
 }
 
+// Work item of the survivor queue: (chunk, triangle lane, image) packed in 32 bits.
+__device__ __forceinline__ int pack_item(int64_t chunk, int t, int k) { return (int)(chunk << 8) | (t << 3) | k; }
+
+// Project one triangle into image k's spin frame (Eqs. 2-4) and, when its beta-extent
+// holds at least one layer, rasterise it.  The same arithmetic decides the cull (in the
+// queue phase) and the rasterisation, so the two can never disagree.
+struct Projected {
+    float x[3], y[3], z[3];
+};
+
+__device__ __forceinline__ void project_z(const Frame &f, const float *v, float *p, float *z) {
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        p[3 * j] = v[3 * j] - f.sx;                     // Eq. 2: translate first
+        p[3 * j + 1] = v[3 * j + 1] - f.sy;
+        p[3 * j + 2] = v[3 * j + 2] - f.sz;
+        z[j] = fmaf(f.czx, p[3 * j], fmaf(f.czy, p[3 * j + 1], f.czz * p[3 * j + 2]));   // T_z
+    }
+}
+
 __global__ void __launch_bounds__(kThreads)
 generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere, int64_t n_chunks,
                 const float *__restrict__ origins, int64_t n, float R, int N, int K,
@@ -150,9 +170,11 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
     __shared__ int list[kListCap];
     __shared__ int list_n;
     __shared__ float cta_sphere[4];
+    __shared__ int queue[kThreads / 32][2 * 32];
 
     int *acc = reinterpret_cast<int *>(smem_raw);        // [K][N][N] difference arrays
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const unsigned lt_mask = (1u << lane) - 1u;
     const int64_t img0 = (int64_t)blockIdx.x * K;
     const int k_valid = (int)min((int64_t)K, n - img0);
 
@@ -195,6 +217,41 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
     g.half_r = 0.5f * R;
     g.row_off = 0.5f * (float)N - 0.5f;
     const float cs_r = cta_sphere[3];
+    int qn = 0;                                          // warp-uniform queue length
+
+    // Drain `cnt` (<= 32) queued (chunk, triangle, image) items with one item per lane.
+    auto drain = [&](int cnt) {
+        __syncwarp();
+        int item = lane < cnt ? queue[warp][lane] : -1;
+        int rest = qn - cnt;
+        int moved = lane < rest ? queue[warp][cnt + lane] : 0;
+        __syncwarp();
+        if (lane < rest) queue[warp][lane] = moved;
+        qn = rest;
+        if (item >= 0) {
+            const int64_t chunk = (int64_t)((unsigned)item >> 8);
+            const int t = (item >> 3) & 31, k = item & 7;
+            const float *src = tri + chunk * 9 * kChunk + t;
+            float v[9];
+#pragma unroll
+            for (int c = 0; c < 9; ++c) v[c] = __ldg(src + c * kChunk);
+            const Frame f = frames[k];
+            float p[9], z[3];
+            project_z(f, v, p, z);
+            float x[3], y[3];
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {                // Eqs. 3-4 for T_x, T_y
+                float qx = fmaf(f.nax, p[3 * j], f.nay * p[3 * j + 1]);
+                y[j] = fmaf(-f.nay, p[3 * j], f.nax * p[3 * j + 1]);
+                x[j] = fmaf(f.nbz, qx, -f.nbx * p[3 * j + 2]);
+            }
+            float ax = x[0], ay = y[0], az = z[0], bx = x[1], by = y[1], bz = z[1],
+                  cx = x[2], cy = y[2], cz = z[2];
+            sort3(ax, ay, az, bx, by, bz, cx, cy, cz);
+            rasterise_triangle(acc + k * N * N, g, ax, ay, az, bx, by, bz, cx, cy, cz);
+        }
+        __syncwarp();
+    };
 
     if (cs_r >= 0.f) {
         const float ccx = cta_sphere[0], ccy = cta_sphere[1], ccz = cta_sphere[2];
@@ -214,7 +271,7 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
                 int pos = 0;
                 if (lane == 0 && m) pos = atomicAdd(&list_n, __popc(m));
                 pos = __shfl_sync(0xffffffffu, pos, 0);
-                if (keep) list[pos + __popc(m & ((1u << lane) - 1u))] = (int)(c - base);
+                if (keep) list[pos + __popc(m & lt_mask)] = (int)(c - base);
             }
             __syncthreads();
             const int cnt = list_n;
@@ -223,42 +280,29 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
                 const float *src = tri + chunk * 9 * kChunk + lane;
                 float v[9];
 #pragma unroll
-                for (int k = 0; k < 9; ++k) v[k] = __ldg(src + k * kChunk);
+                for (int c = 0; c < 9; ++c) v[c] = __ldg(src + c * kChunk);
                 for (int k = 0; k < k_valid; ++k) {
                     const Frame f = frames[k];
-                    if (f.valid == 0.f) continue;
-                    // Eq. 2 (translate) then T_z of Eqs. 3-4 for the beta-extent test
-                    float p[9];
-#pragma unroll
-                    for (int j = 0; j < 3; ++j) {
-                        p[3 * j] = v[3 * j] - f.sx;
-                        p[3 * j + 1] = v[3 * j + 1] - f.sy;
-                        p[3 * j + 2] = v[3 * j + 2] - f.sz;
+                    bool keep = false;
+                    if (f.valid != 0.f) {
+                        // beta-extent test: does any layer centre lie in [z_min, z_max)?
+                        float p[9], z[3];
+                        project_z(f, v, p, z);
+                        float zlo = fminf(z[0], fminf(z[1], z[2])), zhi = fmaxf(z[0], fmaxf(z[1], z[2]));
+                        keep = first_at_or_above(zlo, g.inv_delta, g.row_off, N) <
+                               first_at_or_above(zhi, g.inv_delta, g.row_off, N);
                     }
-                    float z0 = fmaf(f.czx, p[0], fmaf(f.czy, p[1], f.czz * p[2]));
-                    float z1 = fmaf(f.czx, p[3], fmaf(f.czy, p[4], f.czz * p[5]));
-                    float z2 = fmaf(f.czx, p[6], fmaf(f.czy, p[7], f.czz * p[8]));
-                    float zlo = fminf(z0, fminf(z1, z2)), zhi = fmaxf(z0, fmaxf(z1, z2));
-                    int r_lo = first_at_or_above(zlo, g.inv_delta, g.row_off, N);
-                    int r_hi = first_at_or_above(zhi, g.inv_delta, g.row_off, N);
-                    if (r_lo >= r_hi) continue;
-                    // Eqs. 3-4 for T_x, T_y (alpha plane)
-                    float x[3], y[3];
-#pragma unroll
-                    for (int j = 0; j < 3; ++j) {
-                        float qx = fmaf(f.nax, p[3 * j], f.nay * p[3 * j + 1]);
-                        y[j] = fmaf(-f.nay, p[3 * j], f.nax * p[3 * j + 1]);
-                        x[j] = fmaf(f.nbz, qx, -f.nbx * p[3 * j + 2]);
-                    }
-                    float ax = x[0], ay = y[0], az = z0, bx = x[1], by = y[1], bz = z1,
-                          cx = x[2], cy = y[2], cz = z2;
-                    sort3(ax, ay, az, bx, by, bz, cx, cy, cz);
-                    rasterise_triangle(acc + k * N * N, g, ax, ay, az, bx, by, bz, cx, cy, cz);
+                    unsigned m = __ballot_sync(0xffffffffu, keep);
+                    if (keep) queue[warp][qn + __popc(m & lt_mask)] = pack_item(chunk, lane, k);
+                    qn += __popc(m);
+                    if (qn >= 32) drain(32);
                 }
             }
             __syncthreads();
         }
+        if (qn > 0) drain(qn);
     }
+    __syncthreads();
 
     // Epilogue 1: per-row inclusive prefix sum of the difference arrays (warp per row).
     const int cpl = (N + 31) / 32;                 // columns per lane
@@ -319,12 +363,12 @@ cudaError_t launch_generate(const DeviceMesh &m, const float *d_origins, int64_t
     if (n == 0) return cudaSuccess;
     const int K = generate_images_per_cta(N);
     size_t smem = (size_t)K * N * N * sizeof(int);
-    static bool attr_set = false;
-    if (!attr_set) {
+    static size_t attr_smem = 0;
+    if (smem > attr_smem) {
         cudaError_t e = cudaFuncSetAttribute(generate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             200 * 1024);
+                                             (int)smem);
         if (e != cudaSuccess) return e;
-        attr_set = true;
+        attr_smem = smem;
     }
     int64_t blocks = (n + K - 1) / K;
     generate_kernel<<<(unsigned)blocks, kThreads, smem, s>>>(m.tri, m.sphere, m.n_chunks, d_origins,
