@@ -140,6 +140,16 @@ def cpu_baseline(cfg, budget_s: float = 20.0):
             "t_image_s": per_img, "t_comparison_s": per_cmp, "t_step_s": t_step}
 
 
+def segments_per_pair(cfg, k: int = 96) -> float:
+    """S/P for the paper-literal construction work W = 43 P + 40 S + 3 N^2 n,
+    from the oracle's segment counter on a fixed sample of images."""
+    import oracle
+    m = cfg["mesh"]
+    idx = np.linspace(0, m.n_vertices - 1, k).astype(np.int64)
+    r = oracle.rici_generate(m.vertices, m.indices, cfg["origins"][idx], cfg["R"], cfg["N"])
+    return r["segments"] / float(k * m.n_triangles)
+
+
 def run_reference(args):
     """--impl reference: the oracle timed as it stands on the host cores (rank 0 only)."""
     rank = int(os.environ.get("RANK", "0"))
@@ -310,6 +320,14 @@ def run_gpu(args):
                            f"x {n} haystack images per rank",
             "hbm_equivalent_frac": comparisons * 8192 / crss_s / 1e9 / pk.get("hbm_gbs", 6548.8)}
     images_per_s = n_total_hay / (step_ms_max / 1e3)
+    spp = segments_per_pair(cfg)
+    P_pairs = float(n) * m.n_triangles
+    W = 43.0 * P_pairs + 40.0 * spp * P_pairs + 3.0 * N * N * n
+    construction = {"ms": gen_ms, "images_per_s": n / (gen_ms / 1e3),
+                    "paper_literal_ops": W, "segments_per_pair": spp,
+                    "paper_literal_frac": W / (gen_ms / 1e3) / (peak * 1e12),
+                    "note": "W = 43 P + 40 S + 3 N^2 n (brute-force pairs); the exact cull skips "
+                            "provably-zero pairs, so this fraction can exceed 1"}
     cb = cpu_baseline(cfg) if world == 1 and not args.no_cpu_baseline else None
     line = {"metric": METRIC, "value": images_per_s, "unit": "images/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms_max,
@@ -322,7 +340,7 @@ def run_gpu(args):
                        "l2": "flushed between timed steps (256 MB write); haystack 285 MB > L2",
                        "parallelism": f"dp{world}"},
             "comparisons_per_s": comparisons * world / (step_ms_max / 1e3),
-            "construction": {"ms": gen_ms, "images_per_s": n / (gen_ms / 1e3)},
+            "construction": construction,
             "crss": {"ms": crss_ms, "comparisons_per_s": comparisons / crss_s},
             "roofline": roof, "cpu_baseline": cb, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk.summary(), "bench_wall_s": wall}

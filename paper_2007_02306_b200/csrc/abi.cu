@@ -156,6 +156,9 @@ rici_status rici_create_mesh(const float *vertices, int64_t n_vertices, const in
     if (n_chunks > 0) {
         e = cudaMalloc(&mesh->m.tri, sizeof(float) * 9 * rici::kChunk * (size_t)n_chunks);
         if (e == cudaSuccess) e = cudaMalloc(&mesh->m.sphere, sizeof(float4) * (size_t)n_chunks);
+        if (e == cudaSuccess)
+            e = cudaMalloc(&mesh->m.super_sphere,
+                           sizeof(float4) * (size_t)((n_chunks + rici::kSuper - 1) / rici::kSuper));
         if (e != cudaSuccess) { rici_destroy_mesh(mesh); return cuda_fail(e, "mesh allocation"); }
         Staging st(s);
         const void *dv = nullptr, *di = nullptr;
@@ -190,6 +193,7 @@ rici_status rici_destroy_mesh(rici_mesh mesh) {
     if (!mesh) return RICI_OK;
     if (mesh->m.tri) cudaFree(mesh->m.tri);
     if (mesh->m.sphere) cudaFree(mesh->m.sphere);
+    if (mesh->m.super_sphere) cudaFree(mesh->m.super_sphere);
     delete mesh;
     return RICI_OK;
 }

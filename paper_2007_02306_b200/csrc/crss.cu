@@ -30,8 +30,10 @@ namespace {
 
 constexpr int kTileImages = 32;          // one haystack image per lane
 constexpr int kCrssThreads = 1024;
-constexpr int kNeedleChunk = 2048;
-constexpr int kWarpBuf = 512;            // per-warp staged needle entries (int32)
+constexpr int kWarps = kCrssThreads / 32;
+constexpr int kNeedleChunk = 2048;       // needles per work item
+constexpr int kSeg = 128;                // entries per cp.async segment (per warp, double-buffered)
+constexpr int kPad = 8;                  // needle lists are padded to a multiple of 8 entries
 constexpr int kSmallMax = 127;
 constexpr int kPixBits = 14;             // pixel index bits (N <= 128)
 
@@ -70,43 +72,93 @@ crss_pairs_kernel(const uint16_t *__restrict__ needles, int64_t nn, const uint16
 }
 
 // ---------------------------------------------------------------- a9: needle change lists
-// entries[i*cap + e] = (D_n << 14) | pixel, pixel = r*N + c (c >= 1), in pixel order.
+// CSR lists: needle i's entries occupy [off[i], off[i+1]), (D_n << 14) | pixel (c >= 1) in pixel
+// order, then zero entries (D_n 0, pixel 0: column 0 has D_h = 0, the term is 0) and a final
+// MARKER entry (D_n 0, pixel N: column 0 of row 1, also a zero term) -- the list length is
+// the smallest multiple of 8 that leaves room for the marker.  A real entry never has a
+// pixel in column 0, so the marker is unambiguous.
+__device__ __forceinline__ int needle_delta(const uint16_t *a, int p, int N, unsigned &mx) {
+    unsigned v = a[p];
+    mx = max(mx, v);
+    return (p % N != 0) ? (int)v - (int)a[p - 1] : 0;
+}
+
 __global__ void __launch_bounds__(256)
-needle_prepare_kernel(const uint16_t *__restrict__ needles, int64_t nn, int N, int cap,
-                      int *__restrict__ entries, int *__restrict__ n_entries,
-                      unsigned char *__restrict__ small) {
+needle_count_kernel(const uint16_t *__restrict__ needles, int64_t nn, int N,
+                    int64_t *__restrict__ plen, int *__restrict__ n_entries,
+                    unsigned char *__restrict__ small) {
     const int lane = threadIdx.x & 31;
     const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (i >= nn) return;
     const int P = N * N;
     const uint16_t *a = needles + i * (int64_t)P;
-    int *dst = entries + i * (int64_t)cap;
+    int cnt = 0;
+    unsigned mx = 0;
+    for (int base = 0; base < P; base += 32) {
+        int dn = (base + lane < P) ? needle_delta(a, base + lane, N, mx) : 0;
+        cnt += __popc(__ballot_sync(0xffffffffu, dn != 0));
+    }
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) {
+        n_entries[i] = cnt;
+        plen[i] = ((cnt + 1 + kPad - 1) / kPad) * kPad;
+        small[i] = mx <= (unsigned)kSmallMax;
+    }
+}
+
+// exclusive scan of n int64 values in place (one CTA sweeping 1024 at a time); off[n] = total
+__global__ void __launch_bounds__(1024) scan_i64_kernel(int64_t *__restrict__ v, int64_t n) {
+    __shared__ int64_t part[1024];
+    __shared__ int64_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int64_t base = 0; base < n; base += 1024) {
+        const int64_t i = base + threadIdx.x;
+        const int64_t x = i < n ? v[i] : 0;
+        part[threadIdx.x] = x;
+        __syncthreads();
+        for (int o = 1; o < 1024; o <<= 1) {
+            int64_t t = threadIdx.x >= o ? part[threadIdx.x - o] : 0;
+            __syncthreads();
+            part[threadIdx.x] += t;
+            __syncthreads();
+        }
+        const int64_t incl = part[threadIdx.x] + carry;
+        if (i < n) v[i] = incl - x;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry = incl;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) v[n] = carry;
+}
+
+__global__ void __launch_bounds__(256)
+needle_fill_kernel(const uint16_t *__restrict__ needles, int64_t nn, int N,
+                   const int64_t *__restrict__ off, int *__restrict__ entries) {
+    const int lane = threadIdx.x & 31;
+    const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (i >= nn) return;
+    const int P = N * N;
+    const uint16_t *a = needles + i * (int64_t)P;
+    int *dst = entries + off[i];
+    const int len = (int)(off[i + 1] - off[i]);
     int cnt = 0;
     unsigned mx = 0;
     for (int base = 0; base < P; base += 32) {
         int p = base + lane;
-        int dn = 0;
-        if (p < P) {
-            unsigned v = a[p];
-            mx = max(mx, v);
-            if (p % N != 0) dn = (int)v - (int)a[p - 1];
-        }
+        int dn = (p < P) ? needle_delta(a, p, N, mx) : 0;
         unsigned m = __ballot_sync(0xffffffffu, dn != 0);
         if (dn != 0) dst[cnt + __popc(m & ((1u << lane) - 1u))] = dn * (1 << kPixBits) + p;
         cnt += __popc(m);
     }
-    // pad to a multiple of 4 with entry 0 = (D_n 0, pixel 0): column 0 has D_h = 0 in the
-    // staged planes, so a pad entry adds (0 - 0)^2 = 0
-    if (lane < ((4 - (cnt & 3)) & 3)) dst[cnt + lane] = 0;
-    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if (lane == 0) { n_entries[i] = cnt; small[i] = mx <= (unsigned)kSmallMax; }
+    for (int e = cnt + lane; e < len; e += 32) dst[e] = (e == len - 1) ? N : 0;
 }
 
 // ---------------------------------------------------------------- a11 + a12: tiles
 struct TileArgs {
     const uint16_t *hay; int64_t nh;
     const uint16_t *needles; int64_t nn;
-    const int *entries; const int *n_entries; const unsigned char *small; int cap;
+    const int *entries; const int64_t *off; const int *n_entries; const unsigned char *small;
     const uint64_t *thr; uint32_t *counts; uint64_t *dist;
     int N, plane_bytes, use_smem;
     int64_t n_tiles, n_groups, tiles_per_group, n_items;
@@ -129,6 +181,46 @@ __device__ __forceinline__ int sq_term(int entry, unsigned mask, unsigned key) {
     return d * d;
 }
 
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Exact uint64 CRSS of needle list L (n entries) against haystack image h, from global memory.
+__device__ __forceinline__ uint64_t crss_exact(const int *__restrict__ L, int n, const uint16_t *__restrict__ h) {
+    uint64_t acc = 0;
+    for (int e = 0; e < n; ++e) {
+        int v0 = __ldg(L + e);
+        int p = v0 & ((1 << kPixBits) - 1);
+        int64_t dn = v0 >> kPixBits;
+        int64_t dhv = (int64_t)__ldg(h + p) - (int64_t)__ldg(h + p - 1);
+        int64_t df = dn - dhv;
+        acc += (uint64_t)(df * df);
+    }
+    return acc;
+}
+
+// Close needle il for this lane's haystack image (a12): count it when CRSS < t_i (warp ballot +
+// popc into the chunk's shared counters), or write the distance row.  Needles or tiles with
+// a pixel above 127 take the exact 64-bit path here.  Kept out of line: it runs once per
+// (needle, tile) and would otherwise crowd the registers of the entry loop.
+__device__ __noinline__ void finish_needle(const TileArgs &A, int il, int64_t i0, unsigned acc, bool tsmall,
+                                           bool valid, int64_t gj, const uint16_t *hj, unsigned *cnt_s,
+                                           const unsigned *small_s, const uint64_t *thr_s, int lane) {
+    const int64_t gi = i0 + il;
+    uint64_t d = acc;
+    if (!((small_s[il >> 5] >> (il & 31)) & 1u) || !tsmall)
+        d = valid ? crss_exact(A.entries + A.off[gi], A.n_entries[gi], hj) : 0;
+    if (A.thr) {
+        unsigned bm = __ballot_sync(0xffffffffu, valid && d < thr_s[il]);
+        if (lane == 0) cnt_s[il] += __popc(bm);
+    }
+    if (A.dist && valid) A.dist[gi * A.nh + gj] = d;
+}
+
 __global__ void __launch_bounds__(kCrssThreads, 1)
 crss_tile_kernel(TileArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -138,14 +230,18 @@ crss_tile_kernel(TileArgs A) {
     const unsigned pad = S ? ((S - (raw_sh & (S - 1))) & (S - 1)) : 0u;
     unsigned char *dh = smem_raw + pad;
     const unsigned tile_sh = raw_sh + pad;
-    int *wbuf_all = reinterpret_cast<int *>(smem_raw + (S ? S : 16) + kTileImages * S);  // [warps][kWarpBuf]
+    unsigned char *after = smem_raw + (S ? S : 16) + kTileImages * S;
+    int *segbuf_all = reinterpret_cast<int *>(after);                               // [warps][2][kSeg]
+    uint64_t *thr_s = reinterpret_cast<uint64_t *>(after + kWarps * 2 * kSeg * sizeof(int));  // [chunk]
+    int *off_s = reinterpret_cast<int *>(thr_s + kNeedleChunk);   // [chunk+1] list offsets relative to the chunk
     __shared__ unsigned cnt_s[kNeedleChunk];
+    __shared__ unsigned small_s[kNeedleChunk / 32];
+    __shared__ int warp_first[kWarps + 1];
     __shared__ long long item_s;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int nwarps = kCrssThreads / 32;
     const int N = A.N, P = N * N;
-    int *wbuf = wbuf_all + warp * kWarpBuf;
+    int *seg0 = segbuf_all + warp * 2 * kSeg;
     const bool vec_stage = (N % 8) == 0;
 
     for (;;) {
@@ -159,12 +255,45 @@ crss_tile_kernel(TileArgs A) {
         const int nc = (int)min((int64_t)kNeedleChunk, A.nn - i0);
         const int64_t t_begin = group * A.tiles_per_group;
         const int64_t t_end = min(A.n_tiles, t_begin + A.tiles_per_group);
-        for (int i = tid; i < nc; i += kCrssThreads) cnt_s[i] = 0;
+        for (int i = tid; i <= nc; i += kCrssThreads) {
+            off_s[i] = (int)(A.off[i0 + i] - A.off[i0]);
+            if (i < nc) {
+                cnt_s[i] = 0;
+                if (A.thr) thr_s[i] = A.thr[i0 + i];
+            }
+        }
+        for (int w = tid; w < kNeedleChunk / 32; w += kCrssThreads) {
+            unsigned bits = 0;
+            for (int b = 0; b < 32; ++b) {
+                int i = w * 32 + b;
+                if (i < nc && A.small[i0 + i]) bits |= 1u << b;
+            }
+            small_s[w] = bits;
+        }
+        // split the chunk's entry stream into kWarps runs of whole needles with ~equal entries
+        if (tid <= kWarps) {
+            const int64_t e0 = A.off[i0], e1 = A.off[i0 + nc];
+            const int64_t target = e0 + (e1 - e0) * tid / kWarps;
+            int lo = 0, hi = nc;                         // first needle with off >= target
+            while (lo < hi) {
+                int mid = (lo + hi) >> 1;
+                if (A.off[i0 + mid] < target) lo = mid + 1; else hi = mid;
+            }
+            warp_first[tid] = tid == kWarps ? nc : (tid == 0 ? 0 : lo);
+        }
+        __syncthreads();
+        const int wa = warp_first[warp], wb = max(wa, warp_first[warp + 1]);
+        const int64_t s_begin = A.off[i0 + wa], s_end = A.off[i0 + wb];
+        const int n_seg = (int)((s_end - s_begin + kSeg - 1) / kSeg);
 
         for (int64_t tile = t_begin; tile < t_end; ++tile) {
             const int64_t j0 = tile * kTileImages;
             const int nj = (int)min((int64_t)kTileImages, A.nh - j0);
             __syncthreads();                              // previous tile fully consumed
+            // first segment of this warp's needle stream: overlaps with the tile staging
+            if (n_seg > 0 && lane * 4 < kSeg && s_begin + lane * 4 < s_end)
+                cp_async16(seg0 + lane * 4, A.entries + s_begin + lane * 4);
+            cp_async_commit();
             // stage D_h(r,c) = h[r][c] - h[r][c-1] as int8 planes (0 in column 0); the left
             // neighbour of a thread's 8-pixel run comes from the previous lane
             int small_local = 1;
@@ -218,56 +347,53 @@ crss_tile_kernel(TileArgs A) {
             const unsigned key = (tile_sh + (unsigned)lane * S) | ((unsigned)lane << 2);
             const bool valid = lane < nj;
             const int64_t gj = j0 + lane;
-            for (int il = warp; il < nc; il += nwarps) {
-                const int64_t gi = i0 + il;
-                const int ne = A.n_entries[gi];
-                const int *L = A.entries + gi * (int64_t)A.cap;
-                uint64_t d;
-                if (tile_small && A.small[gi]) {
-                    // fast path: |D_n|,|D_h| <= 127 -> every term <= 254^2, sum < 2^32
-                    const int ne4 = (ne + 3) & ~3;
-                    unsigned acc = 0;
-                    for (int s0 = 0; s0 < ne4; s0 += kWarpBuf) {
-                        const int sn = min(kWarpBuf, ne4 - s0);
-                        __syncwarp();
-                        for (int e = lane * 4; e < sn; e += 128)
-                            *reinterpret_cast<int4 *>(wbuf + e) = __ldg(reinterpret_cast<const int4 *>(L + s0 + e));
-                        __syncwarp();
-                        int e = 0;
-                        for (; e + 8 <= sn; e += 8) {
-                            const int4 u = *reinterpret_cast<const int4 *>(wbuf + e);
-                            const int4 v = *reinterpret_cast<const int4 *>(wbuf + e + 4);
-                            acc += (unsigned)(sq_term(u.x, mask, key) + sq_term(u.y, mask, key) + sq_term(u.z, mask, key) + sq_term(u.w, mask, key));
-                            acc += (unsigned)(sq_term(v.x, mask, key) + sq_term(v.y, mask, key) + sq_term(v.z, mask, key) + sq_term(v.w, mask, key));
-                        }
-                        if (e < sn) {
-                            const int4 u = *reinterpret_cast<const int4 *>(wbuf + e);
-                            acc += (unsigned)(sq_term(u.x, mask, key) + sq_term(u.y, mask, key) + sq_term(u.z, mask, key) + sq_term(u.w, mask, key));
-                        }
-                    }
-                    d = acc;
+            const uint16_t *hj = A.hay + (valid ? gj : j0) * (int64_t)P;
+
+            const bool tsmall = tile_small != 0;
+            if (!tile_small) {
+                cp_async_wait<0>();
+                for (int il = wa; il < wb; ++il) finish_needle(A, il, i0, 0, tsmall, valid, gj, hj, cnt_s, small_s, thr_s, lane);
+                continue;
+            }
+            // fast path: the warp's stream in double-buffered segments, consumed in runs that
+            // end at a needle boundary or a segment boundary (both multiples of 8 entries)
+            int il = wa;
+            int rem = wa < wb ? off_s[wa + 1] - off_s[wa] : 0;
+            unsigned acc = 0;
+            for (int k = 0; k < n_seg; ++k) {
+                if (k + 1 < n_seg) {
+                    const int64_t nb = s_begin + (int64_t)(k + 1) * kSeg;
+                    int *dst = seg0 + ((k + 1) & 1) * kSeg;
+                    if (lane * 4 < kSeg && nb + lane * 4 < s_end) cp_async16(dst + lane * 4, A.entries + nb + lane * 4);
+                    cp_async_commit();
+                    cp_async_wait<1>();
                 } else {
-                    // exact 64-bit path straight from global memory
-                    uint64_t acc = 0;
-                    if (valid) {
-                        const uint16_t *h = A.hay + gj * (int64_t)P;
-                        for (int e = 0; e < ne; ++e) {
-                            int v0 = __ldg(L + e);
-                            int p = v0 & ((1 << kPixBits) - 1);
-                            int64_t dn = v0 >> kPixBits;
-                            int64_t dhv = (int64_t)__ldg(h + p) - (int64_t)__ldg(h + p - 1);
-                            int64_t df = dn - dhv;
-                            acc += (uint64_t)(df * df);
-                        }
+                    cp_async_wait<0>();
+                }
+                __syncwarp();
+                const int *buf = seg0 + (k & 1) * kSeg;
+                const int len = (int)min((int64_t)kSeg, s_end - s_begin - (int64_t)k * kSeg);
+                int e = 0;
+                while (e < len) {
+                    const int run = min(rem, len - e);
+                    const int *b = buf + e;
+#pragma unroll 2
+                    for (int q = 0; q < run; q += kPad) {
+                        const int4 u = *reinterpret_cast<const int4 *>(b + q);
+                        const int4 v = *reinterpret_cast<const int4 *>(b + q + 4);
+                        acc += (unsigned)(sq_term(u.x, mask, key) + sq_term(u.y, mask, key) + sq_term(u.z, mask, key) + sq_term(u.w, mask, key));
+                        acc += (unsigned)(sq_term(v.x, mask, key) + sq_term(v.y, mask, key) + sq_term(v.z, mask, key) + sq_term(v.w, mask, key));
                     }
-                    d = acc;
+                    e += run;
+                    rem -= run;
+                    if (rem == 0) {
+                        finish_needle(A, il, i0, acc, tsmall, valid, gj, hj, cnt_s, small_s, thr_s, lane);
+                        acc = 0;
+                        ++il;
+                        rem = il < wb ? off_s[il + 1] - off_s[il] : 0;
+                    }
                 }
-                if (A.thr) {
-                    const uint64_t t = A.thr[gi];
-                    unsigned m = __ballot_sync(0xffffffffu, valid && d < t);
-                    if (lane == 0) cnt_s[il] += __popc(m);
-                }
-                if (A.dist && valid) A.dist[gi * A.nh + gj] = d;
+                __syncwarp();
             }
         }
         __syncthreads();
@@ -302,29 +428,32 @@ cudaError_t launch_crss_search_tiles(const uint16_t *d_needles, int64_t nn,
     }
     if (nn == 0 || nh == 0) return cudaSuccess;
     const int P = N * N;
-    const int cap = ((N * (N - 1) + 3) / 4) * 4;        // int4-aligned list stride
-    int *entries = nullptr, *n_entries = nullptr;
+    // a9: CSR needle change lists
+    int64_t *off = nullptr;
+    int *n_entries = nullptr, *entries = nullptr;
     unsigned char *small = nullptr;
     unsigned long long *work = nullptr;
-    size_t bytes_entries = sizeof(int) * (size_t)cap * nn;
-    if ((e = cudaMallocAsync((void **)&entries, bytes_entries, s)) != cudaSuccess) return e;
+    if ((e = cudaMallocAsync((void **)&off, sizeof(int64_t) * (nn + 1), s)) != cudaSuccess) return e;
     if ((e = cudaMallocAsync((void **)&n_entries, sizeof(int) * nn, s)) != cudaSuccess) return e;
     if ((e = cudaMallocAsync((void **)&small, nn, s)) != cudaSuccess) return e;
     if ((e = cudaMallocAsync((void **)&work, sizeof(unsigned long long), s)) != cudaSuccess) return e;
     if ((e = cudaMemsetAsync(work, 0, sizeof(unsigned long long), s)) != cudaSuccess) return e;
-
-    {
-        const int warps = 8;
-        int64_t blocks = (nn + warps - 1) / warps;
-        needle_prepare_kernel<<<(unsigned)blocks, 32 * warps, 0, s>>>(d_needles, nn, N, cap, entries,
-                                                                      n_entries, small);
-        note_launches(1);
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    }
+    const int warps = 8;
+    const unsigned nb = (unsigned)((nn + warps - 1) / warps);
+    needle_count_kernel<<<nb, 32 * warps, 0, s>>>(d_needles, nn, N, off, n_entries, small);
+    scan_i64_kernel<<<1, 1024, 0, s>>>(off, nn);
+    note_launches(2);
+    // the list sizes are only known on the device: allocate the worst case
+    // (N(N-1) deltas + marker, rounded to 8, per needle) -- stream-ordered, pooled
+    const int64_t cap = ((int64_t)N * (N - 1) + 1 + kPad - 1) / kPad * kPad;
+    if ((e = cudaMallocAsync((void **)&entries, sizeof(int) * cap * nn, s)) != cudaSuccess) return e;
+    needle_fill_kernel<<<nb, 32 * warps, 0, s>>>(d_needles, nn, N, off, entries);
+    note_launches(1);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
 
     TileArgs A;
     A.hay = d_haystack; A.nh = nh; A.needles = d_needles; A.nn = nn;
-    A.entries = entries; A.n_entries = n_entries; A.small = small; A.cap = cap;
+    A.entries = entries; A.off = off; A.n_entries = n_entries; A.small = small;
     A.thr = d_thresholds; A.counts = d_counts; A.dist = d_dist;
     A.N = N;
     int stride = 128;                                    // power of two >= P (XOR swizzle needs >= 128)
@@ -333,7 +462,8 @@ cudaError_t launch_crss_search_tiles(const uint16_t *d_needles, int64_t nn,
     size_t smem = (size_t)(kTileImages + 1) * stride;    // + alignment slack
     A.use_smem = (kTileImages * (size_t)stride <= 128 * 1024) && P < (1 << kPixBits);
     if (!A.use_smem) { smem = 16; A.plane_bytes = 0; }
-    smem += (size_t)(kCrssThreads / 32) * kWarpBuf * sizeof(int);
+    smem += (size_t)kWarps * 2 * kSeg * sizeof(int) + (size_t)kNeedleChunk * sizeof(uint64_t) +
+            (size_t)(kNeedleChunk + 1) * sizeof(int);
     A.n_tiles = (nh + kTileImages - 1) / kTileImages;
     int64_t n_chunks = (nn + kNeedleChunk - 1) / kNeedleChunk;
     int dev = 0, sms = 148;
@@ -358,6 +488,7 @@ cudaError_t launch_crss_search_tiles(const uint16_t *d_needles, int64_t nn,
     note_launches(1);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     cudaFreeAsync(entries, s);
+    cudaFreeAsync(off, s);
     cudaFreeAsync(n_entries, s);
     cudaFreeAsync(small, s);
     cudaFreeAsync(work, s);

@@ -28,7 +28,8 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kMaxK = 8;
-constexpr int kListCap = 4 * kThreads;   // chunk survivors per batch
+constexpr int kListCap = 2 * kThreads;   // superchunk survivors per batch
+constexpr int kChunkCap = 1024;          // chunk survivors per batch (multiple of kSuper)
 
 struct __align__(16) Frame {
     float sx, sy, sz, valid;      // S_v (Eq. 2); valid = 0 for a zero / non-finite normal (G3)
@@ -89,8 +90,11 @@ struct Geometry {
     int n;
 };
 
+__device__ __forceinline__ float fast_sqrt(float x) { return x > 0.f ? x * rsqrtf(x) : 0.f; }
+
 // Steps 1-6 for every layer of one projected, z-sorted triangle, accumulated
-// into the image's per-row difference arrays.
+// into the image's per-row difference arrays.  Approximate reciprocals / square roots
+// (relative error ~1e-7) move decisions by far less than the 1e-5*R attribution bound.
 __device__ __forceinline__ void rasterise_triangle(int *__restrict__ acc, const Geometry &g,
                                                    float ax, float ay, float az, float bx,
                                                    float by, float bz, float cx, float cy,
@@ -98,31 +102,35 @@ __device__ __forceinline__ void rasterise_triangle(int *__restrict__ acc, const 
     const int N = g.n;
     int r_lo = first_at_or_above(az, g.inv_delta, g.row_off, N);
     int r_hi = first_at_or_above(cz, g.inv_delta, g.row_off, N);
+    if (r_lo >= r_hi) return;
+    const float inv_ac = __frcp_rn(cz - az);             // > 0 whenever a layer is inside
+    const float inv_ab = bz > az ? __frcp_rn(bz - az) : 0.f;
+    const float inv_bc = cz > bz ? __frcp_rn(cz - bz) : 0.f;
     for (int r = r_lo; r < r_hi; ++r) {
         float beta = fmaf((float)r + 0.5f, g.delta, -g.half_r);
         if (!(az <= beta && beta < cz)) continue;        // layer membership, half-open (G5)
         // Step 1: E0 on the long edge (a,c), E1 on (a,b) below / (b,c) above the middle vertex.
-        float t = (beta - az) / (cz - az);
+        float t = (beta - az) * inv_ac;
         float e0x = fmaf(t, cx - ax, ax), e0y = fmaf(t, cy - ay, ay);
         float e1x, e1y;
         if (beta < bz) {
-            float u = (beta - az) / (bz - az);
+            float u = (beta - az) * inv_ab;
             e1x = fmaf(u, bx - ax, ax); e1y = fmaf(u, by - ay, ay);
         } else {
-            float u = (beta - bz) / (cz - bz);
+            float u = (beta - bz) * inv_bc;
             e1x = fmaf(u, cx - bx, bx); e1y = fmaf(u, cy - by, by);
         }
         // Step 2: rotate so E0E1 is parallel to x; the normalised direction is (cos, sin).
         float dx = e1x - e0x, dy = e1y - e0y;
         float l2 = dx * dx + dy * dy;
         if (l2 == 0.f) continue;                          // zero-length slice (G5)
-        float len = sqrtf(l2);
-        float cs = dx / len, sn = dy / len;
+        float inv_len = rsqrtf(l2);
+        float cs = dx * inv_len, sn = dy * inv_len;
         float x0 = cs * e0x + sn * e0y;
         float y = -sn * e0x + cs * e0y;
-        float x1 = x0 + len;                              // consistent with the sign test
+        float x1 = x0 + l2 * inv_len;                     // x0 + |E1-E0|: consistent with the sign test
         // Steps 3-4: distances of E0, E1 from the axis; single range [min, max).
-        float r0 = sqrtf(e0x * e0x + e0y * e0y), r1 = sqrtf(e1x * e1x + e1y * e1y);
+        float r0 = fast_sqrt(e0x * e0x + e0y * e0y), r1 = fast_sqrt(e1x * e1x + e1y * e1y);
         int c_min = first_at_or_above(fminf(r0, r1), g.inv_delta, -0.5f, N);
         int c_max = first_at_or_above(fmaxf(r0, r1), g.inv_delta, -0.5f, N);
         int *row = acc + r * N;
@@ -147,10 +155,6 @@ __device__ __forceinline__ int pack_item(int64_t chunk, int t, int k) { return (
 // Project one triangle into image k's spin frame (Eqs. 2-4) and, when its beta-extent
 // holds at least one layer, rasterise it.  The same arithmetic decides the cull (in the
 // queue phase) and the rasterisation, so the two can never disagree.
-struct Projected {
-    float x[3], y[3], z[3];
-};
-
 __device__ __forceinline__ void project_z(const Frame &f, const float *v, float *p, float *z) {
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
@@ -163,12 +167,15 @@ __device__ __forceinline__ void project_z(const Frame &f, const float *v, float 
 
 __global__ void __launch_bounds__(kThreads)
 generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere, int64_t n_chunks,
-                const float *__restrict__ origins, int64_t n, float R, int N, int K,
-                uint16_t *__restrict__ out) {
+                const float4 *__restrict__ super_sphere, int64_t n_super,
+                const float *__restrict__ origins, const int *__restrict__ img_perm, int64_t n,
+                float R, int N, int K, uint16_t *__restrict__ out) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ Frame frames[kMaxK];
+    __shared__ int img_idx[kMaxK];
     __shared__ int list[kListCap];
-    __shared__ int list_n;
+    __shared__ int list_n, list_next, chunk_n;
+    __shared__ int chunk_list[kChunkCap];
     __shared__ float cta_sphere[4];
     __shared__ int queue[kThreads / 32][2 * 32];
 
@@ -180,8 +187,14 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
 
     for (int i = tid; i < K * N * N; i += kThreads) acc[i] = 0;
     if (tid < K) {
-        if (tid < k_valid) frames[tid] = make_frame(origins + 6 * (img0 + tid));
-        else { Frame f = {}; frames[tid] = f; }
+        if (tid < k_valid) {
+            const int idx = img_perm ? img_perm[img0 + tid] : (int)(img0 + tid);
+            img_idx[tid] = idx;
+            frames[tid] = make_frame(origins + 6 * (int64_t)idx);
+        } else {
+            Frame f = {};
+            frames[tid] = f;
+        }
     }
     __syncthreads();
     if (tid == 0) {
@@ -255,16 +268,18 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
 
     if (cs_r >= 0.f) {
         const float ccx = cta_sphere[0], ccy = cta_sphere[1], ccz = cta_sphere[2];
-        for (int64_t base = 0; base < n_chunks; base += kListCap) {
-            if (tid == 0) list_n = 0;
+        const float pad_r = 1e-4f * R;
+        // Level 1: superchunks (kSuper*kChunk triangles) whose sphere meets the CTA sphere.
+        for (int64_t base = 0; base < n_super; base += kListCap) {
+            if (tid == 0) { list_n = 0; list_next = 0; chunk_n = 0; }
             __syncthreads();
             for (int q = 0; q < kListCap / kThreads; ++q) {
                 int64_t c = base + q * kThreads + tid;
                 bool keep = false;
-                if (c < n_chunks) {
-                    float4 s = sphere[c];
-                    float dx = s.x - ccx, dy = s.y - ccy, dz = s.z - ccz;
-                    float rr = s.w + cs_r;
+                if (c < n_super) {
+                    float4 s4 = super_sphere[c];
+                    float dx = s4.x - ccx, dy = s4.y - ccy, dz = s4.z - ccz;
+                    float rr = s4.w + cs_r;
                     keep = dx * dx + dy * dy + dz * dz <= rr * rr;
                 }
                 unsigned m = __ballot_sync(0xffffffffu, keep);
@@ -274,31 +289,76 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
                 if (keep) list[pos + __popc(m & lt_mask)] = (int)(c - base);
             }
             __syncthreads();
-            const int cnt = list_n;
-            for (int e = warp; e < cnt; e += kThreads / 32) {
-                const int64_t chunk = base + list[e];
-                const float *src = tri + chunk * 9 * kChunk + lane;
-                float v[9];
+            const int n_sc = list_n;
+            // Level 2: chunks of the surviving superchunks, in batches that fit the chunk list.
+            for (int sc0 = 0; sc0 < n_sc; sc0 += kChunkCap / kSuper) {
+                const int sc1 = min(n_sc, sc0 + kChunkCap / kSuper);
+                for (int e = sc0 + warp; e < sc1; e += kThreads / 32) {
+                    const int64_t c_lane = (base + list[e]) * kSuper + lane;
+                    bool ck = false;
+                    if (c_lane < n_chunks) {
+                        float4 s4 = sphere[c_lane];
+                        float dx = s4.x - ccx, dy = s4.y - ccy, dz = s4.z - ccz;
+                        float rr = s4.w + cs_r;
+                        ck = dx * dx + dy * dy + dz * dz <= rr * rr;
+                    }
+                    unsigned m = __ballot_sync(0xffffffffu, ck);
+                    int pos = 0;
+                    if (lane == 0 && m) pos = atomicAdd(&chunk_n, __popc(m));
+                    pos = __shfl_sync(0xffffffffu, pos, 0);
+                    if (ck) chunk_list[pos + __popc(m & lt_mask)] = c_lane;
+                }
+                __syncthreads();
+                const int n_ck = chunk_n;
+                // Level 3 (dynamically scheduled, one chunk per warp at a time).
+                for (;;) {
+                    int e = 0;
+                    if (lane == 0) e = atomicAdd(&list_next, 1);
+                    e = __shfl_sync(0xffffffffu, e, 0);
+                    if (e >= n_ck) break;
+                    const int64_t chunk = chunk_list[e];
+                    // images whose support CYLINDER (r <= R, |beta| <= R/2) the chunk sphere meets
+                    unsigned kmask;
+                    {
+                        bool hit = false;
+                        if (lane < k_valid && frames[lane].valid != 0.f) {
+                            const Frame f = frames[lane];
+                            float4 s4 = sphere[chunk];
+                            float dx = s4.x - f.sx, dy = s4.y - f.sy, dz = s4.z - f.sz;
+                            float b = fmaf(f.czx, dx, fmaf(f.czy, dy, f.czz * dz));
+                            float a2 = fmaxf(dx * dx + dy * dy + dz * dz - b * b, 0.f);
+                            float pad = pad_r + 1e-6f * (fabsf(s4.x) + fabsf(s4.y) + fabsf(s4.z) + s4.w);
+                            float ra = R + s4.w + pad;
+                            hit = fabsf(b) <= 0.5f * R + s4.w + pad && a2 <= ra * ra;
+                        }
+                        kmask = __ballot_sync(0xffffffffu, hit);
+                    }
+                    if (kmask == 0) continue;
+                    const float *src = tri + chunk * 9 * kChunk + lane;
+                    float v[9];
 #pragma unroll
-                for (int c = 0; c < 9; ++c) v[c] = __ldg(src + c * kChunk);
-                for (int k = 0; k < k_valid; ++k) {
-                    const Frame f = frames[k];
-                    bool keep = false;
-                    if (f.valid != 0.f) {
-                        // beta-extent test: does any layer centre lie in [z_min, z_max)?
+                    for (int c = 0; c < 9; ++c) v[c] = __ldg(src + c * kChunk);
+                    // (image, triangle) pairs -- beta-extent test: does a layer centre
+                    // lie in [z_min, z_max)?  Survivors go to the warp's queue.
+                    while (kmask) {
+                        const int k = __ffs(kmask) - 1;
+                        kmask &= kmask - 1;
+                        const Frame f = frames[k];
                         float p[9], z[3];
                         project_z(f, v, p, z);
                         float zlo = fminf(z[0], fminf(z[1], z[2])), zhi = fmaxf(z[0], fmaxf(z[1], z[2]));
-                        keep = first_at_or_above(zlo, g.inv_delta, g.row_off, N) <
-                               first_at_or_above(zhi, g.inv_delta, g.row_off, N);
+                        const bool keep = first_at_or_above(zlo, g.inv_delta, g.row_off, N) <
+                                          first_at_or_above(zhi, g.inv_delta, g.row_off, N);
+                        unsigned m = __ballot_sync(0xffffffffu, keep);
+                        if (keep) queue[warp][qn + __popc(m & lt_mask)] = pack_item(chunk, lane, k);
+                        qn += __popc(m);
+                        if (qn >= 32) drain(32);
                     }
-                    unsigned m = __ballot_sync(0xffffffffu, keep);
-                    if (keep) queue[warp][qn + __popc(m & lt_mask)] = pack_item(chunk, lane, k);
-                    qn += __popc(m);
-                    if (qn >= 32) drain(32);
                 }
+                __syncthreads();
+                if (tid == 0) { chunk_n = 0; list_next = 0; }
+                __syncthreads();
             }
-            __syncthreads();
         }
         if (qn > 0) drain(qn);
     }
@@ -329,24 +389,28 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
     }
     __syncthreads();
 
-    // Epilogue 2: saturate to uint16 (G9) and store; 128-bit stores when aligned.
+    // Epilogue 2: saturate to uint16 (G9) and store each image at its caller index;
+    // 128-bit stores when aligned.
     const int npix = N * N;
-    const int64_t total = (int64_t)k_valid * npix;
-    uint16_t *dst = out + img0 * npix;
     const unsigned *cnt = reinterpret_cast<const unsigned *>(acc);
-    if ((npix % 8) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-        for (int64_t i = (int64_t)tid * 8; i < total; i += kThreads * 8) {
-            uint4 a = *reinterpret_cast<const uint4 *>(cnt + i);
-            uint4 b = *reinterpret_cast<const uint4 *>(cnt + i + 4);
-            uint4 o;
-            o.x = min(a.x, 65535u) | (min(a.y, 65535u) << 16);
-            o.y = min(a.z, 65535u) | (min(a.w, 65535u) << 16);
-            o.z = min(b.x, 65535u) | (min(b.y, 65535u) << 16);
-            o.w = min(b.z, 65535u) | (min(b.w, 65535u) << 16);
-            *reinterpret_cast<uint4 *>(dst + i) = o;
+    const bool vec = (npix % 8) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+    for (int k = 0; k < k_valid; ++k) {
+        uint16_t *dst = out + (int64_t)img_idx[k] * npix;
+        const unsigned *src = cnt + k * npix;
+        if (vec) {
+            for (int i = tid * 8; i < npix; i += kThreads * 8) {
+                uint4 a = *reinterpret_cast<const uint4 *>(src + i);
+                uint4 b = *reinterpret_cast<const uint4 *>(src + i + 4);
+                uint4 o;
+                o.x = min(a.x, 65535u) | (min(a.y, 65535u) << 16);
+                o.y = min(a.z, 65535u) | (min(a.w, 65535u) << 16);
+                o.z = min(b.x, 65535u) | (min(b.y, 65535u) << 16);
+                o.w = min(b.z, 65535u) | (min(b.w, 65535u) << 16);
+                *reinterpret_cast<uint4 *>(dst + i) = o;
+            }
+        } else {
+            for (int i = tid; i < npix; i += kThreads) dst[i] = (uint16_t)min(src[i], 65535u);
         }
-    } else {
-        for (int64_t i = tid; i < total; i += kThreads) dst[i] = (uint16_t)min(cnt[i], 65535u);
     }
 }
 
@@ -370,11 +434,18 @@ cudaError_t launch_generate(const DeviceMesh &m, const float *d_origins, int64_t
         if (e != cudaSuccess) return e;
         attr_smem = smem;
     }
+    // build the images in spatial order so a CTA's K support volumes are compact
+    int *perm = nullptr;
+    cudaError_t e = cudaMallocAsync((void **)&perm, sizeof(int) * n, s);
+    if (e != cudaSuccess) return e;
+    if ((e = spatial_order(d_origins, 6, n, perm, s)) != cudaSuccess) return e;
     int64_t blocks = (n + K - 1) / K;
-    generate_kernel<<<(unsigned)blocks, kThreads, smem, s>>>(m.tri, m.sphere, m.n_chunks, d_origins,
-                                                             n, R, N, K, d_out);
+    generate_kernel<<<(unsigned)blocks, kThreads, smem, s>>>(m.tri, m.sphere, m.n_chunks, m.super_sphere,
+                                                             m.n_super, d_origins, perm, n, R, N, K, d_out);
     note_launches(1);
-    return cudaGetLastError();
+    e = cudaGetLastError();
+    cudaFreeAsync(perm, s);
+    return e;
 }
 
 }  // namespace rici

@@ -10,14 +10,20 @@ namespace rici {
 // tri[(chunk*9 + k)*kChunk + lane], k = 0..8 -> v0.x v0.y v0.z v1.x ... v2.z.
 // A warp loads one chunk with 9 fully coalesced 128-byte loads.
 constexpr int kChunk = 32;
+constexpr int kSuper = 32;   // chunks per superchunk (two-level cull hierarchy)
 
 struct DeviceMesh {
-    int64_t nt = 0;          // triangles
-    int64_t n_chunks = 0;    // ceil(nt / kChunk)
-    float *tri = nullptr;    // [n_chunks][9][kChunk]
-    float4 *sphere = nullptr;// [n_chunks] bounding sphere (cx, cy, cz, r) of each chunk
+    int64_t nt = 0;               // triangles
+    int64_t n_chunks = 0;         // ceil(nt / kChunk)
+    int64_t n_super = 0;          // ceil(n_chunks / kSuper)
+    float *tri = nullptr;         // [n_chunks][9][kChunk], triangles in spatial (Morton-cell) order
+    float4 *sphere = nullptr;     // [n_chunks] bounding sphere (cx, cy, cz, r) of each chunk
+    float4 *super_sphere = nullptr;  // [n_super] bounding sphere of each superchunk
     int device = 0;
 };
+
+// perm[k] = index of the k-th of n points (stride floats apart) in spatial order.
+cudaError_t spatial_order(const float *d_pts, int stride, int64_t n, int *d_perm, cudaStream_t s);
 
 // Kernel-launch bookkeeping (rici_launch_count()).
 void note_launches(int k);

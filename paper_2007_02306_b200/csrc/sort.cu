@@ -1,0 +1,138 @@
+// sort.cu -- spatial ordering used by mesh staging (triangles) and construction (images).
+//
+// Not part of the paper's arithmetic: a RICI is a sum over triangles, so the order in
+// which triangles are visited, and the order in which images are built, cannot change
+// any count.  Ordering only makes consecutive triangles (a chunk) and consecutive images
+// (a CTA's group) spatially compact, which is what makes the exact bounding-sphere cull
+// in generate.cu effective for arbitrarily ordered inputs.
+//
+// Method: counting sort of points by an 18-bit Morton code (6 bits per axis over the
+// points' bounding box): histogram (atomics), single-CTA exclusive scan, scatter.
+#include <algorithm>
+
+#include "rici_internal.cuh"
+
+namespace rici {
+namespace {
+
+constexpr int kCellBits = 6;
+constexpr int kCells = 1 << (3 * kCellBits);
+
+__device__ __forceinline__ int ordered(float x) {
+    int i = __float_as_int(x);
+    return i >= 0 ? i : (i ^ 0x7fffffff);
+}
+__device__ __forceinline__ float unordered(int i) { return __int_as_float(i >= 0 ? i : (i ^ 0x7fffffff)); }
+
+__global__ void bbox_init_kernel(int *box) {
+    if (threadIdx.x < 3) box[threadIdx.x] = 0x7fffffff;
+    else if (threadIdx.x < 6) box[threadIdx.x] = (int)0x80000000;
+}
+
+__global__ void __launch_bounds__(256)
+bbox_kernel(const float *__restrict__ pts, int stride, int64_t n, int *__restrict__ box) {
+    int lo[3] = {0x7fffffff, 0x7fffffff, 0x7fffffff};
+    int hi[3] = {(int)0x80000000, (int)0x80000000, (int)0x80000000};
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        for (int a = 0; a < 3; ++a) {
+            float v = pts[i * stride + a];
+            if (!isfinite(v)) continue;
+            int o = ordered(v);
+            lo[a] = min(lo[a], o);
+            hi[a] = max(hi[a], o);
+        }
+    }
+    for (int a = 0; a < 3; ++a) {
+        for (int o = 16; o > 0; o >>= 1) {
+            lo[a] = min(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+            hi[a] = max(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+        }
+        if ((threadIdx.x & 31) == 0) { atomicMin(box + a, lo[a]); atomicMax(box + 3 + a, hi[a]); }
+    }
+}
+
+__device__ __forceinline__ unsigned spread3(unsigned x) {   // 6 bits -> every third bit
+    unsigned r = 0;
+    for (int b = 0; b < kCellBits; ++b) r |= ((x >> b) & 1u) << (3 * b);
+    return r;
+}
+
+__device__ __forceinline__ unsigned cell_of(const float *p, const int *box) {
+    unsigned c[3];
+    for (int a = 0; a < 3; ++a) {
+        float lo = unordered(box[a]), hi = unordered(box[3 + a]);
+        float ext = hi - lo;
+        float t = (ext > 0.f && isfinite(p[a])) ? (p[a] - lo) / ext : 0.f;
+        int q = (int)(t * (float)(1 << kCellBits));
+        c[a] = (unsigned)min(max(q, 0), (1 << kCellBits) - 1);
+    }
+    return spread3(c[0]) | (spread3(c[1]) << 1) | (spread3(c[2]) << 2);
+}
+
+__global__ void __launch_bounds__(256)
+hist_kernel(const float *__restrict__ pts, int stride, int64_t n, const int *__restrict__ box,
+            unsigned *__restrict__ cell, int *__restrict__ hist) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        unsigned c = cell_of(pts + i * stride, box);
+        cell[i] = c;
+        atomicAdd(hist + c, 1);
+    }
+}
+
+// exclusive scan of kCells ints by one CTA of 1024 threads
+__global__ void __launch_bounds__(1024) scan_kernel(int *__restrict__ hist) {
+    constexpr int per = kCells / 1024;
+    __shared__ int sums[1024];
+    int base = threadIdx.x * per;
+    int s = 0;
+    for (int i = 0; i < per; ++i) s += hist[base + i];
+    sums[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {
+        int v = threadIdx.x >= o ? sums[threadIdx.x - o] : 0;
+        __syncthreads();
+        sums[threadIdx.x] += v;
+        __syncthreads();
+    }
+    int run = sums[threadIdx.x] - s;
+    for (int i = 0; i < per; ++i) {
+        int h = hist[base + i];
+        hist[base + i] = run;
+        run += h;
+    }
+}
+
+__global__ void __launch_bounds__(256)
+scatter_kernel(const unsigned *__restrict__ cell, int64_t n, int *__restrict__ offs, int *__restrict__ perm) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        perm[atomicAdd(offs + cell[i], 1)] = (int)i;
+}
+
+}  // namespace
+
+// perm[k] = index of the k-th point in Morton-cell order.  pts: n points, `stride` floats apart.
+// Workspace is stream-ordered.
+cudaError_t spatial_order(const float *d_pts, int stride, int64_t n, int *d_perm, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    cudaError_t e;
+    int *box = nullptr, *hist = nullptr;
+    unsigned *cell = nullptr;
+    if ((e = cudaMallocAsync((void **)&box, 6 * sizeof(int), s)) != cudaSuccess) return e;
+    if ((e = cudaMallocAsync((void **)&hist, kCells * sizeof(int), s)) != cudaSuccess) return e;
+    if ((e = cudaMallocAsync((void **)&cell, n * sizeof(unsigned), s)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(hist, 0, kCells * sizeof(int), s)) != cudaSuccess) return e;
+    int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+    bbox_init_kernel<<<1, 32, 0, s>>>(box);
+    bbox_kernel<<<blocks, 256, 0, s>>>(d_pts, stride, n, box);
+    hist_kernel<<<blocks, 256, 0, s>>>(d_pts, stride, n, box, cell, hist);
+    scan_kernel<<<1, 1024, 0, s>>>(hist);
+    scatter_kernel<<<blocks, 256, 0, s>>>(cell, n, hist, d_perm);
+    note_launches(5);
+    e = cudaGetLastError();
+    cudaFreeAsync(box, s);
+    cudaFreeAsync(hist, s);
+    cudaFreeAsync(cell, s);
+    return e;
+}
+
+}  // namespace rici

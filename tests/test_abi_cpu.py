@@ -66,3 +66,16 @@ def test_product_does_not_touch_oracle():
                 assert not re.search(r"^\s*(import|from)\s+oracle\b", txt, re.M), f
                 assert "librici_oracle" not in txt and "rici_oracle.c" not in txt, f
                 assert not re.search(r"#include\s*[<\"].*oracle", txt), f
+
+
+def test_bench_reference_arm_prints_contract_line():
+    """bench.py --impl reference runs the oracle on the host (no GPU) and prints one JSON line."""
+    import json
+    import sys
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                          "--steps", "1", "--warmup", "0"], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["unit"] == "images/s" and line["value"] > 0
+    assert line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"]["h2d_bytes_per_step"] == 0

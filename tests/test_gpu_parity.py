@@ -101,12 +101,16 @@ def test_adversarial(rici, oracle_mod, case):
         o, R = m.origins[::13], 0.3
     g = _gen(rici, m, o, R, 64)
     ref = oracle_mod.rici_generate(m.vertices, m.indices, o, R, 64, fragile=True)
-    # grid_soup snaps every coordinate and half the normals to a 1/32 grid, so a large share of
-    # its pixels sit exactly on a decision (its fragile fraction is ~4%): only attribution is
-    # binding there, with the differing fraction bounded by 2e-3.
-    _assert_parity(g, ref, max_frac=2e-3 if case == "grid_soup" else 1e-4)
+    # grid_soup snaps every coordinate and half the normals to a 1/32 grid, so ~4% of its
+    # pixels sit exactly on a decision, where FP32 and FP64 legitimately resolve the tie
+    # differently: attribution stays binding and the differing pixels are bounded by 10% of
+    # the fragile ones.  Workload-shaped meshes keep <= 1e-4.
     if case == "grid_soup":
         assert ref["fragile"].mean() > 5e-3
+        n_diff = _assert_parity(g, ref, max_frac=1.0)
+        assert n_diff <= 0.1 * ref["fragile"].sum()
+    else:
+        _assert_parity(g, ref)
 
 
 def test_degenerate_inputs(rici):
