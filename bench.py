@@ -300,38 +300,56 @@ def run_gpu(args):
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel (CRSS count kernel: integer ALU bound)
+    # ---- roofline of the dominant kernel: the tcgen05 int8 GEMM that ranks all pairs
+    # (DESIGN.md 6.2).  Algorithmic ops per comparison = 2 x K with K = 2 x 4096 int8 features;
+    # peak = the measured bf16 dense burst x 2 (nominal int8 : bf16 ratio on B200).
     pk, src = peaks()
     sm_mhz = pk.get("sm_max_mhz", 1965.0)
     imgs_np = imgs.cpu().numpy().view(np.uint16)
-    d = np.diff(imgs_np.astype(np.int32), axis=2)
-    nnz = int((d != 0).sum())                                 # sum over needles of |mask|
-    n_total_hay = n * world
-    terms = float(nnz) * n_total_hay / world                  # per rank: every needle x local shard
     comparisons = float(imgs_np.shape[0]) * n                # per rank
+    n_total_hay = n * world
     crss_s = crss_ms / 1e3
-    achieved = terms * CRSS_OPS_PER_TERM / crss_s / 1e12      # Tops/s
-    peak = SMS * LANES_PER_SM * sm_mhz * 1e6 / 1e12
-    roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s",
-            "frac": achieved / peak, "traffic": None,
-            "kernel": "crss_tile_kernel (+needle prepare, thresholds; timed as the rici_crss_search call)",
-            "peak_source": f"{SMS} SMs x {LANES_PER_SM} INT32 lanes x sm_max {sm_mhz} MHz ({src} clock)",
-            "algorithmic": f"{CRSS_OPS_PER_TERM} int ops per masked term; {nnz} masked needle terms "
-                           f"x {n} haystack images per rank",
-            "hbm_equivalent_frac": comparisons * 8192 / crss_s / 1e9 / pk.get("hbm_gbs", 6548.8)}
+    mma = os.environ.get("RICI_CRSS_PATH", "") != "simt"
+    if mma:
+        K = 2 * 4096
+        achieved = comparisons * 2.0 * K / crss_s / 1e12          # Tops/s (int8)
+        peak = 2.0 * pk.get("bf16_tflops", 1587.6)
+        roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": None,
+                "kernel": "crss_mma_kernel (tcgen05.mma kind::i8, TMA, TMEM) timed as the whole "
+                          "rici_crss_search call (features, thresholds, fallback bookkeeping included)",
+                "dtype": "int8 x int8 -> int32",
+                "peak_source": f"{src} bf16 dense burst {pk.get('bf16_tflops', 1587.6)} TFLOP/s x 2 "
+                               "(nominal int8/bf16 ratio 4.5/2.25 PFLOP/s)",
+                "algorithmic": f"2 x {K} int8 MACs per comparison x {comparisons:.0f} comparisons",
+                "nominal_frac": achieved / 4500.0}
+    else:
+        d = np.diff(imgs_np.astype(np.int32), axis=2)
+        nnz = int((d != 0).sum())
+        terms = float(nnz) * n
+        achieved = terms * CRSS_OPS_PER_TERM / crss_s / 1e12
+        peak = SMS * LANES_PER_SM * sm_mhz * 1e6 / 1e12
+        roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s",
+                "frac": achieved / peak, "traffic": None,
+                "kernel": "crss_tile_kernel (SIMT; timed as the rici_crss_search call)",
+                "peak_source": f"{SMS} SMs x {LANES_PER_SM} INT32 lanes x sm_max {sm_mhz} MHz ({src} clock)",
+                "algorithmic": f"{CRSS_OPS_PER_TERM} int ops per masked term; {nnz} masked needle terms "
+                               f"x {n} haystack images per rank"}
+    roof["hbm_equivalent_frac"] = comparisons * 8192 / crss_s / 1e9 / pk.get("hbm_gbs", 6548.8)
     images_per_s = n_total_hay / (step_ms_max / 1e3)
     spp = segments_per_pair(cfg)
+    alu_peak = SMS * LANES_PER_SM * sm_mhz * 1e6 / 1e12
     P_pairs = float(n) * m.n_triangles
     W = 43.0 * P_pairs + 40.0 * spp * P_pairs + 3.0 * N * N * n
     construction = {"ms": gen_ms, "images_per_s": n / (gen_ms / 1e3),
                     "paper_literal_ops": W, "segments_per_pair": spp,
-                    "paper_literal_frac": W / (gen_ms / 1e3) / (peak * 1e12),
+                    "paper_literal_frac": W / (gen_ms / 1e3) / (alu_peak * 1e12),
                     "note": "W = 43 P + 40 S + 3 N^2 n (brute-force pairs); the exact cull skips "
                             "provably-zero pairs, so this fraction can exceed 1"}
     cb = cpu_baseline(cfg) if world == 1 and not args.no_cpu_baseline else None
     line = {"metric": METRIC, "value": images_per_s, "unit": "images/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms_max,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32/i32",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32/i8",
             "data": "synthetic",
             "config": {"workload": "C2: bumpy torus 264x132 (T=69,696), RICI 64x64 at all 34,848 "
                                    "vertices, R=0.3, CRSS self-search 34,848 x 34,848"

@@ -76,7 +76,8 @@ RICI_API rici_status rici_create_mesh(const float *vertices, int64_t n_vertices,
                              const int32_t *indices, int64_t n_triangles,
                              rici_stream_t stream, rici_mesh *out_mesh);
 
-/* Frees the mesh (cudaFree: waits for outstanding work on the device).  NULL is a no-op. */
+/* Frees the mesh: stream-ordered release on the legacy default stream, i.e. after all
+ * previously enqueued work on blocking streams; does not block the host.  NULL is a no-op. */
 RICI_API rici_status rici_destroy_mesh(rici_mesh mesh);
 
 /* Number of triangles in the mesh, or -1 for NULL. */
@@ -106,7 +107,12 @@ RICI_API rici_status rici_generate(rici_mesh mesh, const float *origins, int64_t
  *   needles    [n_needles][N][N] uint16
  *   haystack   [n_haystack][N][N] uint16, n_haystack >= n_needles
  *   out_ranks  [n_needles] uint32
- * Exact integer arithmetic (bit-exact for every input).                       */
+ * Exact integer arithmetic (bit-exact for every input).
+ * Kernels: for n_bins = 64 the counts run on the tensor cores (tcgen05 int8 GEMM of the
+ * expanded Eq. 7, exact under a per-image guard |D_n| <= 63, |D_h| <= 15) and the few images
+ * outside the guard are recounted by the SIMT kernel; this sizing step synchronises `stream`
+ * once.  Other n_bins, or RICI_CRSS_PATH=simt in the environment, use the SIMT kernel only
+ * (no synchronisation).  rici_crss_count_below follows the same rule.                    */
 RICI_API rici_status rici_crss_search(const uint16_t *needles, int64_t n_needles,
                              const uint16_t *haystack, int64_t n_haystack,
                              int32_t n_bins, uint32_t *out_ranks, rici_stream_t stream);

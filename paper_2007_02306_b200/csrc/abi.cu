@@ -5,6 +5,7 @@
 #include <new>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -19,6 +20,14 @@ struct rici_mesh_s {
 namespace rici {
 static std::atomic<unsigned long long> g_launches{0};
 void note_launches(int k) { g_launches.fetch_add((unsigned long long)k, std::memory_order_relaxed); }
+bool use_mma_path(int N) {
+    static int mode = -1;                  // 1 = tensor cores where applicable, 0 = SIMT only
+    if (mode < 0) {
+        const char *v = getenv("RICI_CRSS_PATH");
+        mode = (v && strcmp(v, "simt") == 0) ? 0 : 1;
+    }
+    return mode == 1 && N == 64;
+}
 }  // namespace rici
 
 namespace {
@@ -118,6 +127,18 @@ struct Staging {
 
 bool valid_bins(int32_t n_bins) { return n_bins >= 2 && n_bins <= 128; }
 
+// a9-a12 counts: tensor-core path for N = 64 (exact, with SIMT fallback inside), else SIMT.
+cudaError_t count_below(const void *dn, int64_t nn, const void *dh, int64_t nh, int N, const uint64_t *thr,
+                        uint32_t *counts, cudaStream_t s) {
+    if (rici::use_mma_path(N)) {
+        cudaError_t e = rici::launch_crss_count_mma((const uint16_t *)dn, nn, (const uint16_t *)dh, nh, thr, counts, s);
+        if (e != cudaErrorNotSupported) return e;
+        cudaGetLastError();
+    }
+    return rici::launch_crss_search_tiles((const uint16_t *)dn, nn, (const uint16_t *)dh, nh, N, thr, counts,
+                                          nullptr, s);
+}
+
 rici_status check_images(const void *p, int64_t n, const char *name) {
     if (n < 0) return fail(RICI_ERR_INVALID_ARGUMENT, "%s: negative count %lld", name, (long long)n);
     if (n > 0 && p == nullptr) return fail(RICI_ERR_INVALID_ARGUMENT, "%s: null pointer", name);
@@ -154,11 +175,12 @@ rici_status rici_create_mesh(const float *vertices, int64_t n_vertices, const in
     int64_t n_chunks = (n_triangles + rici::kChunk - 1) / rici::kChunk;
     cudaError_t e = cudaSuccess;
     if (n_chunks > 0) {
-        e = cudaMalloc(&mesh->m.tri, sizeof(float) * 9 * rici::kChunk * (size_t)n_chunks);
-        if (e == cudaSuccess) e = cudaMalloc(&mesh->m.sphere, sizeof(float4) * (size_t)n_chunks);
+        // stream-ordered pool allocations: no device-wide synchronisation on create/destroy
+        e = cudaMallocAsync((void **)&mesh->m.tri, sizeof(float) * 9 * rici::kChunk * (size_t)n_chunks, s);
+        if (e == cudaSuccess) e = cudaMallocAsync((void **)&mesh->m.sphere, sizeof(float4) * (size_t)n_chunks, s);
         if (e == cudaSuccess)
-            e = cudaMalloc(&mesh->m.super_sphere,
-                           sizeof(float4) * (size_t)((n_chunks + rici::kSuper - 1) / rici::kSuper));
+            e = cudaMallocAsync((void **)&mesh->m.super_sphere,
+                                sizeof(float4) * (size_t)((n_chunks + rici::kSuper - 1) / rici::kSuper), s);
         if (e != cudaSuccess) { rici_destroy_mesh(mesh); return cuda_fail(e, "mesh allocation"); }
         Staging st(s);
         const void *dv = nullptr, *di = nullptr;
@@ -191,9 +213,11 @@ rici_status rici_create_mesh(const float *vertices, int64_t n_vertices, const in
 rici_status rici_destroy_mesh(rici_mesh mesh) {
     g_err.clear();
     if (!mesh) return RICI_OK;
-    if (mesh->m.tri) cudaFree(mesh->m.tri);
-    if (mesh->m.sphere) cudaFree(mesh->m.sphere);
-    if (mesh->m.super_sphere) cudaFree(mesh->m.super_sphere);
+    // ordered after all prior work on the legacy default stream (which every blocking stream,
+    // including the creation stream, synchronises with)
+    if (mesh->m.tri) cudaFreeAsync(mesh->m.tri, 0);
+    if (mesh->m.sphere) cudaFreeAsync(mesh->m.sphere, 0);
+    if (mesh->m.super_sphere) cudaFreeAsync(mesh->m.super_sphere, 0);
     delete mesh;
     return RICI_OK;
 }
@@ -279,10 +303,8 @@ rici_status rici_crss_count_below(const uint16_t *needles, int64_t n_needles,
     if (e == cudaSuccess) e = st.in(haystack, sizeof(uint16_t) * P * n_haystack, &dh);
     if (e == cudaSuccess) e = st.in(thresholds, sizeof(uint64_t) * (size_t)n_needles, &dt);
     if (e == cudaSuccess) e = st.out(out_counts, sizeof(uint32_t) * (size_t)n_needles, &dc);
-    if (e == cudaSuccess)
-        e = rici::launch_crss_search_tiles((const uint16_t *)dn, n_needles, (const uint16_t *)dh,
-                                           n_haystack, n_bins, (const uint64_t *)dt, (uint32_t *)dc,
-                                           nullptr, s);
+    if (e == cudaSuccess) e = count_below(dn, n_needles, dh, n_haystack, n_bins, (const uint64_t *)dt,
+                                          (uint32_t *)dc, s);
     if (e == cudaSuccess) e = st.finish();
     if (e != cudaSuccess) return cuda_fail(e, "rici_crss_count_below");
     return RICI_OK;
@@ -343,9 +365,7 @@ rici_status rici_crss_search(const uint16_t *needles, int64_t n_needles, const u
         e = rici::launch_crss_pairs((const uint16_t *)dn, n_needles, (const uint16_t *)dh, n_haystack,
                                     n_bins, nullptr, n_needles, thr, s);
     }
-    if (e == cudaSuccess)
-        e = rici::launch_crss_search_tiles((const uint16_t *)dn, n_needles, (const uint16_t *)dh,
-                                           n_haystack, n_bins, thr, (uint32_t *)dr, nullptr, s);
+    if (e == cudaSuccess) e = count_below(dn, n_needles, dh, n_haystack, n_bins, thr, (uint32_t *)dr, s);
     if (e == cudaSuccess) e = st.finish();
     if (e != cudaSuccess) return cuda_fail(e, "rici_crss_search");
     return RICI_OK;

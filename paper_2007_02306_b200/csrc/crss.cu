@@ -59,13 +59,44 @@ crss_pairs_kernel(const uint16_t *__restrict__ needles, int64_t nn, const uint16
     const int64_t P = (int64_t)N * N;
     const uint16_t *a = needles + i * P, *b = hay + j * P;
     uint64_t acc = 0;
-    for (int p = lane; p < P; p += 32) {
-        if (p % N == 0) continue;                        // "Skip first column" (Listing 1)
-        int64_t dn = (int64_t)a[p] - (int64_t)a[p - 1];
-        if (dn == 0) continue;                           // only where the needle changes
-        int64_t dh = (int64_t)b[p] - (int64_t)b[p - 1];
-        int64_t d = dn - dh;
-        acc += (uint64_t)(d * d);
+    if ((N % 8) == 0) {
+        // 8 pixels per lane per step (16-byte loads); the left neighbour of a run is the
+        // previous lane's last pixel (P:497 shuffle), or the row's own first pixel at column 0
+        for (int64_t base = 0; base < P; base += 256) {       // warp-uniform trip count
+            const int64_t p0 = base + 8 * lane;
+            const bool live = p0 < P;
+            uint4 wa = make_uint4(0, 0, 0, 0), wb = make_uint4(0, 0, 0, 0);
+            if (live) {
+                wa = __ldg(reinterpret_cast<const uint4 *>(a + p0));
+                wb = __ldg(reinterpret_cast<const uint4 *>(b + p0));
+            }
+            const unsigned pa = __shfl_up_sync(0xffffffffu, wa.w, 1), pb = __shfl_up_sync(0xffffffffu, wb.w, 1);
+            if (!live) continue;
+            int xa[8] = {(int)(wa.x & 0xffff), (int)(wa.x >> 16), (int)(wa.y & 0xffff), (int)(wa.y >> 16),
+                         (int)(wa.z & 0xffff), (int)(wa.z >> 16), (int)(wa.w & 0xffff), (int)(wa.w >> 16)};
+            int xb[8] = {(int)(wb.x & 0xffff), (int)(wb.x >> 16), (int)(wb.y & 0xffff), (int)(wb.y >> 16),
+                         (int)(wb.z & 0xffff), (int)(wb.z >> 16), (int)(wb.w & 0xffff), (int)(wb.w >> 16)};
+            int la, lb;
+            if (p0 % N == 0) { la = xa[0]; lb = xb[0]; }
+            else if (lane == 0) { la = a[p0 - 1]; lb = b[p0 - 1]; }
+            else { la = (int)(pa >> 16); lb = (int)(pb >> 16); }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int64_t dn = (int64_t)xa[k] - (k ? xa[k - 1] : la);
+                if (dn == 0) continue;                   // only where the needle changes
+                const int64_t dh = (int64_t)xb[k] - (k ? xb[k - 1] : lb);
+                acc += (uint64_t)((dn - dh) * (dn - dh));
+            }
+        }
+    } else {
+        for (int p = lane; p < P; p += 32) {
+            if (p % N == 0) continue;                    // "Skip first column" (Listing 1)
+            int64_t dn = (int64_t)a[p] - (int64_t)a[p - 1];
+            if (dn == 0) continue;                       // only where the needle changes
+            int64_t dh = (int64_t)b[p] - (int64_t)b[p - 1];
+            int64_t d = dn - dh;
+            acc += (uint64_t)(d * d);
+        }
     }
     acc = warp_sum_u64(acc);
     if (lane == 0) out[k] = acc;

@@ -47,4 +47,12 @@ cudaError_t launch_crss_search_tiles(const uint16_t *d_needles, int64_t nn,
                                      const uint64_t *d_thresholds, uint32_t *d_counts,
                                      uint64_t *d_dist, cudaStream_t s);
 
+// a9-a12 on the tensor cores (N = 64): rank counts with the int8 tcgen05 GEMM formulation,
+// exact fallback to the SIMT kernel for images outside the int8 guard.
+cudaError_t launch_crss_count_mma(const uint16_t *d_needles, int64_t nn, const uint16_t *d_haystack, int64_t nh,
+                                  const uint64_t *d_thr, uint32_t *d_counts, cudaStream_t s);
+
+// Which kernel counts ranks: the tensor-core path when N == 64 and RICI_CRSS_PATH != "simt".
+bool use_mma_path(int N);
+
 }  // namespace rici

@@ -7,7 +7,7 @@
 // in generate.cu effective for arbitrarily ordered inputs.
 //
 // Method: counting sort of points by an 18-bit Morton code (6 bits per axis over the
-// points' bounding box): histogram (atomics), single-CTA exclusive scan, scatter.
+// points' bounding box): histogram (atomics), three-pass exclusive scan, scatter.
 #include <algorithm>
 
 #include "rici_internal.cuh"
@@ -79,27 +79,46 @@ hist_kernel(const float *__restrict__ pts, int stride, int64_t n, const int *__r
     }
 }
 
-// exclusive scan of kCells ints by one CTA of 1024 threads
-__global__ void __launch_bounds__(1024) scan_kernel(int *__restrict__ hist) {
-    constexpr int per = kCells / 1024;
-    __shared__ int sums[1024];
-    int base = threadIdx.x * per;
-    int s = 0;
-    for (int i = 0; i < per; ++i) s += hist[base + i];
-    sums[threadIdx.x] = s;
+// exclusive scan of kCells ints: per-block scans, a scan of the block totals, a fix-up pass
+__device__ __forceinline__ int block_exclusive_scan_1024(int v, int *warp_tot) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int incl = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) warp_tot[warp] = incl;
     __syncthreads();
-    for (int o = 1; o < 1024; o <<= 1) {
-        int v = threadIdx.x >= o ? sums[threadIdx.x - o] : 0;
-        __syncthreads();
-        sums[threadIdx.x] += v;
-        __syncthreads();
+    if (warp == 0) {
+        int w = warp_tot[lane], wi = w;
+        for (int o = 1; o < 32; o <<= 1) {
+            int t = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += t;
+        }
+        warp_tot[lane] = wi - w;                  // exclusive prefix of warp totals
     }
-    int run = sums[threadIdx.x] - s;
-    for (int i = 0; i < per; ++i) {
-        int h = hist[base + i];
-        hist[base + i] = run;
-        run += h;
-    }
+    __syncthreads();
+    return incl - v + warp_tot[warp];
+}
+
+__global__ void __launch_bounds__(1024) scan_blocks_kernel(int *__restrict__ hist, int *__restrict__ sums) {
+    __shared__ int warp_tot[32];
+    const int i = blockIdx.x * 1024 + threadIdx.x;
+    const int v = hist[i];
+    const int ex = block_exclusive_scan_1024(v, warp_tot);
+    hist[i] = ex;
+    if (threadIdx.x == 1023) sums[blockIdx.x] = ex + v;
+}
+
+__global__ void __launch_bounds__(1024) scan_sums_kernel(int *__restrict__ sums, int n) {
+    __shared__ int warp_tot[32];
+    const int v = threadIdx.x < n ? sums[threadIdx.x] : 0;
+    const int ex = block_exclusive_scan_1024(v, warp_tot);
+    if (threadIdx.x < n) sums[threadIdx.x] = ex;
+}
+
+__global__ void __launch_bounds__(1024) scan_add_kernel(int *__restrict__ hist, const int *__restrict__ sums) {
+    hist[blockIdx.x * 1024 + threadIdx.x] += sums[blockIdx.x];
 }
 
 __global__ void __launch_bounds__(256)
@@ -115,23 +134,28 @@ scatter_kernel(const unsigned *__restrict__ cell, int64_t n, int *__restrict__ o
 cudaError_t spatial_order(const float *d_pts, int stride, int64_t n, int *d_perm, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     cudaError_t e;
-    int *box = nullptr, *hist = nullptr;
+    static_assert(kCells % 1024 == 0 && kCells / 1024 <= 1024, "scan layout");
+    int *box = nullptr, *hist = nullptr, *sums = nullptr;
     unsigned *cell = nullptr;
     if ((e = cudaMallocAsync((void **)&box, 6 * sizeof(int), s)) != cudaSuccess) return e;
     if ((e = cudaMallocAsync((void **)&hist, kCells * sizeof(int), s)) != cudaSuccess) return e;
     if ((e = cudaMallocAsync((void **)&cell, n * sizeof(unsigned), s)) != cudaSuccess) return e;
+    if ((e = cudaMallocAsync((void **)&sums, (kCells / 1024) * sizeof(int), s)) != cudaSuccess) return e;
     if ((e = cudaMemsetAsync(hist, 0, kCells * sizeof(int), s)) != cudaSuccess) return e;
     int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
     bbox_init_kernel<<<1, 32, 0, s>>>(box);
     bbox_kernel<<<blocks, 256, 0, s>>>(d_pts, stride, n, box);
     hist_kernel<<<blocks, 256, 0, s>>>(d_pts, stride, n, box, cell, hist);
-    scan_kernel<<<1, 1024, 0, s>>>(hist);
+    scan_blocks_kernel<<<kCells / 1024, 1024, 0, s>>>(hist, sums);
+    scan_sums_kernel<<<1, 1024, 0, s>>>(sums, kCells / 1024);
+    scan_add_kernel<<<kCells / 1024, 1024, 0, s>>>(hist, sums);
     scatter_kernel<<<blocks, 256, 0, s>>>(cell, n, hist, d_perm);
-    note_launches(5);
+    note_launches(7);
     e = cudaGetLastError();
     cudaFreeAsync(box, s);
     cudaFreeAsync(hist, s);
     cudaFreeAsync(cell, s);
+    cudaFreeAsync(sums, s);
     return e;
 }
 

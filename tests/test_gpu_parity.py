@@ -237,3 +237,50 @@ def test_ranks_ties_and_duplicates(rici, oracle_mod):
     H = np.concatenate([A, A[::-1], _rand_imgs(rng, 29, hi=3, density=0.05)])   # duplicates -> ties
     r = rici.rici_crss_search(_dev(A), _dev(H)).cpu().numpy()
     assert np.array_equal(r.astype(np.uint32), oracle_mod.ranks(A, H))
+
+
+# ------------------------------------------------------------------ tensor-core path (N = 64)
+def _mixed_images(rng, k, hi_small, n_big, big):
+    a = _rand_imgs(rng, k, hi=hi_small, density=0.3)
+    for q in rng.choice(k, n_big, replace=False):             # break the int8 guard
+        a[q, rng.integers(0, 64), rng.integers(1, 64)] = big
+    return a
+
+
+@pytest.mark.parametrize("big", [16, 70, 300, 65535])
+def test_crss_count_mma_guard_and_fallback(rici, oracle_mod, big):
+    """Counts through the tcgen05 path: ragged M/N tiles (300 needles, 777 haystack images),
+    images whose |D| breaks the int8 guard (|D_n| > 63 or |D_h| > 15) recounted by the SIMT
+    path -- the union must equal the oracle exactly."""
+    rng = np.random.default_rng(big)
+    A = _mixed_images(rng, 300, 9, 7, big)
+    H = np.concatenate([A, _mixed_images(rng, 477, 9, 11, big)])
+    D = oracle_mod.crss_matrix(A, H)
+    thr = D[np.arange(300), rng.integers(0, H.shape[0], 300)].copy()
+    got = rici.rici_crss_count_below(_dev(A), _dev(H), torch.from_numpy(thr.view(np.int64)).to(DEV))
+    assert np.array_equal(got.cpu().numpy().astype(np.int64), (D < thr[:, None]).sum(1))
+    r = rici.rici_crss_search(_dev(A), _dev(H)).cpu().numpy()
+    assert np.array_equal(r.astype(np.uint32), oracle_mod.ranks(A, H))
+
+
+def test_crss_paths_agree_subprocess(tmp_path):
+    """The SIMT path (RICI_CRSS_PATH=simt) and the tensor-core path give identical ranks."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import numpy as np, torch, sys; sys.path.insert(0, %r)\n"
+        "import synth, paper_2007_02306_b200 as r\n"
+        "m = synth.bumpy_torus(120, 60, key=(31,))\n"
+        "mesh = r.rici_create_mesh(torch.from_numpy(m.vertices).cuda(), torch.from_numpy(m.indices).cuda())\n"
+        "im = r.rici_generate(mesh, torch.from_numpy(m.origins).cuda(), 0.3, 64)\n"
+        "ranks = r.rici_crss_search(im[:2000], im).cpu().numpy()\n"
+        "np.save(sys.argv[1], ranks)\n") % root
+    outs = {}
+    for path in ("simt", "mma"):
+        env = dict(os.environ, RICI_CRSS_PATH=path)
+        f = str(tmp_path / f"{path}.npy")
+        subprocess.run([sys.executable, "-c", code, f], env=env, check=True, timeout=600)
+        outs[path] = np.load(f)
+    assert np.array_equal(outs["simt"], outs["mma"])
