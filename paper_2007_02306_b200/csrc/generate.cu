@@ -85,7 +85,7 @@ __device__ __forceinline__ void sort3(float &ax, float &ay, float &az, float &bx
 }
 
 struct Geometry {
-    float delta, inv_delta, half_r;
+    float delta, inv_delta, half_r, r2;
     float row_off;     // (R/2)/delta - 1/2 : row index = ceil(beta*inv_delta + row_off)
     int n;
 };
@@ -228,6 +228,7 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
     g.delta = R / (float)N;
     g.inv_delta = (float)N / R;
     g.half_r = 0.5f * R;
+    g.r2 = R * R;
     g.row_off = 0.5f * (float)N - 0.5f;
     const float cs_r = cta_sphere[3];
     int qn = 0;                                          // warp-uniform queue length
@@ -258,10 +259,16 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
                 y[j] = fmaf(-f.nay, p[3 * j], f.nax * p[3 * j + 1]);
                 x[j] = fmaf(f.nbz, qx, -f.nbx * p[3 * j + 2]);
             }
-            float ax = x[0], ay = y[0], az = z[0], bx = x[1], by = y[1], bz = z[1],
-                  cx = x[2], cy = y[2], cz = z[2];
-            sort3(ax, ay, az, bx, by, bz, cx, cy, cz);
-            rasterise_triangle(acc + k * N * N, g, ax, ay, az, bx, by, bz, cx, cy, cz);
+            // alpha cull: if the triangle's (T_x, T_y) bounding box misses the disk of radius R,
+            // every slice point has alpha > R > rho_{N-1} and no bin can be hit (exact skip)
+            const float bx0 = fmaxf(fmaxf(fminf(x[0], fminf(x[1], x[2])), -fmaxf(x[0], fmaxf(x[1], x[2]))), 0.f);
+            const float by0 = fmaxf(fmaxf(fminf(y[0], fminf(y[1], y[2])), -fmaxf(y[0], fmaxf(y[1], y[2]))), 0.f);
+            if (bx0 * bx0 + by0 * by0 <= g.r2) {
+                float ax = x[0], ay = y[0], az = z[0], bx = x[1], by = y[1], bz = z[1],
+                      cx = x[2], cy = y[2], cz = z[2];
+                sort3(ax, ay, az, bx, by, bz, cx, cy, cz);
+                rasterise_triangle(acc + k * N * N, g, ax, ay, az, bx, by, bz, cx, cy, cz);
+            }
         }
         __syncwarp();
     };
