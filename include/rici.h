@@ -117,6 +117,20 @@ RICI_API rici_status rici_crss_search(const uint16_t *needles, int64_t n_needles
                              const uint16_t *haystack, int64_t n_haystack,
                              int32_t n_bins, uint32_t *out_ranks, rici_stream_t stream);
 
+/* rici_crss_search with options.  flags:
+ *   RICI_CRSS_SIMT        use the SIMT kernel even for n_bins = 64 (no synchronisation)
+ *   RICI_CRSS_EARLY_EXIT  rank mode ("cease execution when a predetermined distance
+ *                         threshold is exceeded"): a needle's accumulation over a group of 32
+ *                         haystack images stops once every partial sum is >= t_i.  Partial
+ *                         sums only grow, so the ranks are identical (G12); implies
+ *                         RICI_CRSS_SIMT.  Needle entries are visited in decreasing |D_n|.  */
+#define RICI_CRSS_SIMT 1u
+#define RICI_CRSS_EARLY_EXIT 2u
+RICI_API rici_status rici_crss_search_ex(const uint16_t *needles, int64_t n_needles,
+                                         const uint16_t *haystack, int64_t n_haystack,
+                                         int32_t n_bins, uint32_t flags, uint32_t *out_ranks,
+                                         rici_stream_t stream);
+
 /* Sharding primitives (used by the multi-GPU layer).
  * rici_crss_pairs: out[k] = CRSS(needles[pairs[k][0]], haystack[pairs[k][1]]).
  *   pairs [m][2] int64 (needle index, haystack index).  With HOST pairs every

@@ -19,7 +19,7 @@ import torch
 from ._lib import RiciError, check, load
 
 __all__ = ["Mesh", "RiciError", "rici_create_mesh", "rici_destroy_mesh", "rici_generate",
-           "rici_crss_search", "rici_crss_pairs", "rici_crss_count_below", "rici_crss_distances",
+           "rici_crss_search", "rici_crss_search_ex", "rici_crss_pairs", "rici_crss_count_below", "rici_crss_distances",
            "rici_launch_count", "rici_version", "library_path"]
 
 
@@ -137,18 +137,32 @@ def _bins_of(x) -> int:
     return int(x.shape[-1])
 
 
-def rici_crss_search(needles, haystack, n_bins: int | None = None, out=None, stream=None) -> torch.Tensor:
-    """(a9-a12) ``rici_crss_search``: ranks with needle i <-> haystack i.  Returns an int32
-    tensor holding the uint32 ranks (on the needles' device, or pinned host memory)."""
+def rici_crss_search(needles, haystack, n_bins: int | None = None, out=None, stream=None,
+                     early_exit: bool = False, simt: bool = False) -> torch.Tensor:
+    """(a9-a12) ``rici_crss_search`` / ``rici_crss_search_ex``: ranks with needle i <-> haystack i.
+    ``early_exit`` selects rank mode (identical ranks), ``simt`` forces the SIMT kernel.
+    Returns an int32 tensor holding the uint32 ranks (needles' device, or pinned host memory)."""
+    from ._lib import RICI_CRSS_EARLY_EXIT, RICI_CRSS_SIMT
     N = n_bins or _bins_of(needles)
     nd, nn = _images(needles, N)
     hd, nh = _images(haystack, N)
     if out is None:
         out = torch.empty(nn, dtype=torch.int32, device=nd.device,
                           pin_memory=(not nd.is_cuda and torch.cuda.is_available()))
-    check(load().rici_crss_search(_ptr(nd), nn, _ptr(hd), nh, N, _ptr(out),
-                                  ctypes.c_void_p(_stream(stream))))
+    flags = (RICI_CRSS_EARLY_EXIT if early_exit else 0) | (RICI_CRSS_SIMT if simt else 0)
+    if flags:
+        check(load().rici_crss_search_ex(_ptr(nd), nn, _ptr(hd), nh, N, flags, _ptr(out),
+                                         ctypes.c_void_p(_stream(stream))))
+    else:
+        check(load().rici_crss_search(_ptr(nd), nn, _ptr(hd), nh, N, _ptr(out),
+                                      ctypes.c_void_p(_stream(stream))))
     return out
+
+
+def rici_crss_search_ex(needles, haystack, flags: int, n_bins: int | None = None, out=None, stream=None):
+    """``rici_crss_search_ex`` with raw flags (RICI_CRSS_SIMT = 1, RICI_CRSS_EARLY_EXIT = 2)."""
+    return rici_crss_search(needles, haystack, n_bins, out, stream, early_exit=bool(flags & 2),
+                            simt=bool(flags & 1))
 
 
 def rici_crss_pairs(needles, haystack, pairs, n_bins: int | None = None, out=None, stream=None) -> torch.Tensor:

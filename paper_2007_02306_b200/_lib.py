@@ -13,8 +13,11 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "librici.so")
 
 SYMBOLS = ["rici_create_mesh", "rici_destroy_mesh", "rici_mesh_num_triangles", "rici_generate",
-           "rici_crss_search", "rici_crss_pairs", "rici_crss_count_below", "rici_crss_distances",
+           "rici_crss_search", "rici_crss_search_ex", "rici_crss_pairs", "rici_crss_count_below", "rici_crss_distances",
            "rici_last_error", "rici_launch_count", "rici_version"]
+
+RICI_CRSS_SIMT = 1
+RICI_CRSS_EARLY_EXIT = 2
 
 STATUS = {0: "RICI_OK", 1: "RICI_ERR_INVALID_ARGUMENT", 2: "RICI_ERR_CUDA",
           3: "RICI_ERR_OUT_OF_MEMORY", 4: "RICI_ERR_UNSUPPORTED"}
@@ -48,6 +51,8 @@ def load() -> ctypes.CDLL:
     lib.rici_generate.restype = st
     lib.rici_crss_search.argtypes = [P, i64, P, i64, i32, P, P]
     lib.rici_crss_search.restype = st
+    lib.rici_crss_search_ex.argtypes = [P, i64, P, i64, i32, ctypes.c_uint32, P, P]
+    lib.rici_crss_search_ex.restype = st
     lib.rici_crss_pairs.argtypes = [P, i64, P, i64, i32, P, i64, P, P]
     lib.rici_crss_pairs.restype = st
     lib.rici_crss_count_below.argtypes = [P, i64, P, i64, i32, P, P, P]

@@ -1,0 +1,121 @@
+"""Clutterbox experiment harness on synthetic objects.
+
+The protocol, step by step:
+  1. a clutterbox of side s (default 3);
+  2. n objects (here seeded synthetic bumpy tori instead of SHREC2017, which is not available);
+  3. each normalised to the unit sphere;
+  4. the reference object is object 0;
+  5. reference descriptors {RD}: one RICI per unique vertex of the reference object alone;
+  6. objects are placed one at a time (reference first), each at a uniform random rotation
+     and a centre in [1, s-1]^3 (G15); after each configured clutter level the cluttered
+     descriptors {CD} of the combined mesh are generated and every d in {RD} is ranked
+     against {CD} -- the correspondence is vertex i <-> scene vertex i because the reference
+     is placed first (G11); "lower ranks are better", ties take the best rank;
+  7. one rank histogram per clutter level; the paper plots the rank-0 fraction.
+
+All descriptor and rank work runs through the C ABI (rici_create_mesh / rici_generate /
+rici_crss_search); this module only assembles scenes and histograms.
+
+    python -m paper_2007_02306_b200.clutterbox --scenes 4 --levels 1,5,10 --grid 120,60
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+_ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if _ROOT not in sys.path:
+    sys.path.insert(0, _ROOT)
+
+
+def rank_histogram(ranks: np.ndarray, n_haystack: int) -> dict:
+    """Histogram of ranks (bin i = how often the correct vertex was found at rank i),
+    sparse: {rank: count}; plus the rank-0 fraction the paper plots."""
+    r = np.asarray(ranks, dtype=np.int64)
+    if r.size and (r.min() < 0 or r.max() > n_haystack - 1):
+        raise ValueError("rank outside [0, |CD|-1] (P:388)")
+    vals, cnts = np.unique(r, return_counts=True)
+    return {"counts": {int(v): int(c) for v, c in zip(vals, cnts)}, "total": int(r.size),
+            "rank0_fraction": float((r == 0).mean()) if r.size else 0.0}
+
+
+def build_scene_objects(scene: int, n_objects: int, grid=(120, 60)):
+    """Seeded synthetic objects for one scene (unit-sphere bumpy tori, varied minor radius)."""
+    import synth
+    objs = []
+    for k in range(n_objects):
+        rng = synth.rng_for(5, scene, k, 99)
+        objs.append(synth.bumpy_torus(grid[0], grid[1], key=(5, scene, k),
+                                      minor=float(rng.uniform(0.2, 0.45)), amp=0.08))
+    return objs
+
+
+def run_scene(scene: int, levels, grid=(120, 60), box_side: float = 3.0, R: float = 0.3, N: int = 64,
+              generate=None, search=None):
+    """One clutterbox run: returns {level: histogram} plus timing.  `generate(mesh, origins)` and
+    `search(needles, haystack)` default to the CUDA library."""
+    import synth
+    if generate is None or search is None:
+        import torch
+
+        import paper_2007_02306_b200 as rici
+
+        def generate(mesh, origins):  # noqa: F811
+            m = rici.rici_create_mesh(torch.from_numpy(mesh.vertices).cuda(), torch.from_numpy(mesh.indices).cuda())
+            out = rici.rici_generate(m, torch.from_numpy(origins).cuda(), R, N)
+            m.destroy()
+            return out
+
+        def search(needles, haystack):  # noqa: F811
+            return rici.rici_crss_search(needles, haystack).cpu().numpy()
+    levels = sorted(set(int(x) for x in levels))
+    objs = build_scene_objects(scene, max(levels), grid)
+    placed = synth.clutterbox(objs, key=(5, scene, 1000), box_side=box_side)
+    n_ref = objs[0].n_vertices
+    # {RD}: the reference object alone, in its placed pose (RICI is rigid-invariant)
+    ref = synth.Mesh(placed.vertices[:n_ref].copy(), objs[0].indices.copy(), placed.normals[:n_ref].copy())
+    t0 = time.perf_counter()
+    rd = generate(ref, ref.origins)
+    out = {"scene": scene, "n_reference_vertices": n_ref, "levels": {}}
+    v_off = np.cumsum([0] + [o.n_vertices for o in objs])
+    t_off = np.cumsum([0] + [o.n_triangles for o in objs])
+    for lv in levels:
+        nv, nt = int(v_off[lv]), int(t_off[lv])
+        sc = synth.Mesh(placed.vertices[:nv], placed.indices[:nt], placed.normals[:nv])
+        cd = generate(sc, sc.origins)                      # {CD} of the combined mesh
+        ranks = search(rd, cd)
+        h = rank_histogram(ranks, nv)
+        h.update({"n_objects": lv, "n_scene_vertices": nv, "n_scene_triangles": nt,
+                  "comparisons": int(n_ref) * nv})
+        out["levels"][lv] = h
+    out["seconds"] = time.perf_counter() - t0
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--scenes", type=int, default=2)
+    ap.add_argument("--levels", default="1,5,10")
+    ap.add_argument("--grid", default="120,60", help="torus grid per object (nu,nv)")
+    ap.add_argument("--out", default=None)
+    a = ap.parse_args()
+    levels = [int(x) for x in a.levels.split(",")]
+    grid = tuple(int(x) for x in a.grid.split(","))
+    res = [run_scene(s, levels, grid) for s in range(a.scenes)]
+    summary = {lv: float(np.mean([r["levels"][lv]["rank0_fraction"] for r in res])) for lv in levels}
+    doc = {"protocol": "clutterbox (P:379-391), synthetic tori", "levels": levels, "grid": grid,
+           "mean_rank0_fraction": summary, "runs": res}
+    txt = json.dumps(doc, indent=1, default=str)
+    if a.out:
+        with open(a.out, "w") as f:
+            f.write(txt)
+    print(json.dumps({"mean_rank0_fraction": summary, "seconds": sum(r["seconds"] for r in res)}))
+
+
+if __name__ == "__main__":
+    main()

@@ -336,9 +336,9 @@ rici_status rici_crss_distances(const uint16_t *needles, int64_t n_needles,
     return RICI_OK;
 }
 
-rici_status rici_crss_search(const uint16_t *needles, int64_t n_needles, const uint16_t *haystack,
-                             int64_t n_haystack, int32_t n_bins, uint32_t *out_ranks,
-                             rici_stream_t stream) {
+rici_status rici_crss_search_ex(const uint16_t *needles, int64_t n_needles, const uint16_t *haystack,
+                                int64_t n_haystack, int32_t n_bins, uint32_t flags, uint32_t *out_ranks,
+                                rici_stream_t stream) {
     g_err.clear();
     if (!valid_bins(n_bins)) return fail(RICI_ERR_INVALID_ARGUMENT, "n_bins must be in [2,128]");
     if (rici_status st = check_images(needles, n_needles, "needles")) return st;
@@ -347,6 +347,7 @@ rici_status rici_crss_search(const uint16_t *needles, int64_t n_needles, const u
         return fail(RICI_ERR_INVALID_ARGUMENT, "n_haystack (%lld) < n_needles (%lld): needle i "
                     "corresponds to haystack i", (long long)n_haystack, (long long)n_needles);
     if (n_needles > 0 && !out_ranks) return fail(RICI_ERR_INVALID_ARGUMENT, "null out_ranks");
+    if (flags & ~(RICI_CRSS_SIMT | RICI_CRSS_EARLY_EXIT)) return fail(RICI_ERR_INVALID_ARGUMENT, "unknown flags");
     if (rici_status st = check_device()) return st;
     if (n_needles == 0) return RICI_OK;
     cudaStream_t s = (cudaStream_t)stream;
@@ -365,10 +366,23 @@ rici_status rici_crss_search(const uint16_t *needles, int64_t n_needles, const u
         e = rici::launch_crss_pairs((const uint16_t *)dn, n_needles, (const uint16_t *)dh, n_haystack,
                                     n_bins, nullptr, n_needles, thr, s);
     }
-    if (e == cudaSuccess) e = count_below(dn, n_needles, dh, n_haystack, n_bins, thr, (uint32_t *)dr, s);
+    if (e == cudaSuccess) {
+        if (flags & (RICI_CRSS_SIMT | RICI_CRSS_EARLY_EXIT))
+            e = rici::launch_crss_search_tiles((const uint16_t *)dn, n_needles, (const uint16_t *)dh, n_haystack,
+                                               n_bins, thr, (uint32_t *)dr, nullptr, s,
+                                               (flags & RICI_CRSS_EARLY_EXIT) != 0);
+        else
+            e = count_below(dn, n_needles, dh, n_haystack, n_bins, thr, (uint32_t *)dr, s);
+    }
     if (e == cudaSuccess) e = st.finish();
     if (e != cudaSuccess) return cuda_fail(e, "rici_crss_search");
     return RICI_OK;
+}
+
+rici_status rici_crss_search(const uint16_t *needles, int64_t n_needles, const uint16_t *haystack,
+                             int64_t n_haystack, int32_t n_bins, uint32_t *out_ranks,
+                             rici_stream_t stream) {
+    return rici_crss_search_ex(needles, n_needles, haystack, n_haystack, n_bins, 0u, out_ranks, stream);
 }
 
 }  // extern "C"

@@ -173,14 +173,21 @@ needle_fill_kernel(const uint16_t *__restrict__ needles, int64_t nn, int N,
     const uint16_t *a = needles + i * (int64_t)P;
     int *dst = entries + off[i];
     const int len = (int)(off[i + 1] - off[i]);
+    // entries in decreasing-|D_n| buckets (the sum is order-independent; large terms first make
+    // the rank-mode early exit trigger sooner)
+    const int lo_b[5] = {8, 4, 3, 2, 1}, hi_b[5] = {1 << 30, 7, 3, 2, 1};
     int cnt = 0;
     unsigned mx = 0;
-    for (int base = 0; base < P; base += 32) {
-        int p = base + lane;
-        int dn = (p < P) ? needle_delta(a, p, N, mx) : 0;
-        unsigned m = __ballot_sync(0xffffffffu, dn != 0);
-        if (dn != 0) dst[cnt + __popc(m & ((1u << lane) - 1u))] = dn * (1 << kPixBits) + p;
-        cnt += __popc(m);
+    for (int bk = 0; bk < 5; ++bk) {
+        for (int base = 0; base < P; base += 32) {
+            int p = base + lane;
+            int dn = (p < P) ? needle_delta(a, p, N, mx) : 0;
+            const int ad = abs(dn);
+            const bool take = dn != 0 && ad >= lo_b[bk] && ad <= hi_b[bk];
+            unsigned m = __ballot_sync(0xffffffffu, take);
+            if (take) dst[cnt + __popc(m & ((1u << lane) - 1u))] = dn * (1 << kPixBits) + p;
+            cnt += __popc(m);
+        }
     }
     for (int e = cnt + lane; e < len; e += 32) dst[e] = (e == len - 1) ? N : 0;
 }
@@ -191,7 +198,7 @@ struct TileArgs {
     const uint16_t *needles; int64_t nn;
     const int *entries; const int64_t *off; const int *n_entries; const unsigned char *small;
     const uint64_t *thr; uint32_t *counts; uint64_t *dist;
-    int N, plane_bytes, use_smem;
+    int N, plane_bytes, use_smem, early_exit;
     int64_t n_tiles, n_groups, tiles_per_group, n_items;
     unsigned long long *work;
 };
@@ -391,6 +398,9 @@ crss_tile_kernel(TileArgs A) {
             int il = wa;
             int rem = wa < wb ? off_s[wa + 1] - off_s[wa] : 0;
             unsigned acc = 0;
+            const bool early = A.early_exit != 0;
+            bool dead = false;                                // rank mode: every lane already >= t_i
+            uint64_t t_cur = (early && wa < wb) ? thr_s[wa] : 0;
             for (int k = 0; k < n_seg; ++k) {
                 if (k + 1 < n_seg) {
                     const int64_t nb = s_begin + (int64_t)(k + 1) * kSeg;
@@ -408,20 +418,34 @@ crss_tile_kernel(TileArgs A) {
                 while (e < len) {
                     const int run = min(rem, len - e);
                     const int *b = buf + e;
+                    if (!early) {
 #pragma unroll 2
-                    for (int q = 0; q < run; q += kPad) {
-                        const int4 u = *reinterpret_cast<const int4 *>(b + q);
-                        const int4 v = *reinterpret_cast<const int4 *>(b + q + 4);
-                        acc += (unsigned)(sq_term(u.x, mask, key) + sq_term(u.y, mask, key) + sq_term(u.z, mask, key) + sq_term(u.w, mask, key));
-                        acc += (unsigned)(sq_term(v.x, mask, key) + sq_term(v.y, mask, key) + sq_term(v.z, mask, key) + sq_term(v.w, mask, key));
+                        for (int q = 0; q < run; q += kPad) {
+                            const int4 u = *reinterpret_cast<const int4 *>(b + q);
+                            const int4 v = *reinterpret_cast<const int4 *>(b + q + 4);
+                            acc += (unsigned)(sq_term(u.x, mask, key) + sq_term(u.y, mask, key) + sq_term(u.z, mask, key) + sq_term(u.w, mask, key));
+                            acc += (unsigned)(sq_term(v.x, mask, key) + sq_term(v.y, mask, key) + sq_term(v.z, mask, key) + sq_term(v.w, mask, key));
+                        }
+                    } else if (!dead) {
+                        // partial sums only grow, so once every lane is >= t_i the
+                        // needle's remaining terms cannot change any count (G12)
+                        for (int q = 0; q < run; q += kPad) {
+                            const int4 u = *reinterpret_cast<const int4 *>(b + q);
+                            const int4 v = *reinterpret_cast<const int4 *>(b + q + 4);
+                            acc += (unsigned)(sq_term(u.x, mask, key) + sq_term(u.y, mask, key) + sq_term(u.z, mask, key) + sq_term(u.w, mask, key));
+                            acc += (unsigned)(sq_term(v.x, mask, key) + sq_term(v.y, mask, key) + sq_term(v.z, mask, key) + sq_term(v.w, mask, key));
+                            if (__all_sync(0xffffffffu, !valid || (uint64_t)acc >= t_cur)) { dead = true; break; }
+                        }
                     }
                     e += run;
                     rem -= run;
                     if (rem == 0) {
                         finish_needle(A, il, i0, acc, tsmall, valid, gj, hj, cnt_s, small_s, thr_s, lane);
                         acc = 0;
+                        dead = false;
                         ++il;
                         rem = il < wb ? off_s[il + 1] - off_s[il] : 0;
+                        if (early && il < wb) t_cur = thr_s[il];
                     }
                 }
                 __syncwarp();
@@ -451,7 +475,7 @@ cudaError_t launch_crss_pairs(const uint16_t *d_needles, int64_t nn, const uint1
 cudaError_t launch_crss_search_tiles(const uint16_t *d_needles, int64_t nn,
                                      const uint16_t *d_haystack, int64_t nh, int N,
                                      const uint64_t *d_thresholds, uint32_t *d_counts,
-                                     uint64_t *d_dist, cudaStream_t s) {
+                                     uint64_t *d_dist, cudaStream_t s, bool early_exit) {
     cudaError_t e;
     if (d_counts && nn > 0) {
         e = cudaMemsetAsync(d_counts, 0, sizeof(uint32_t) * nn, s);
@@ -487,6 +511,7 @@ cudaError_t launch_crss_search_tiles(const uint16_t *d_needles, int64_t nn,
     A.entries = entries; A.off = off; A.n_entries = n_entries; A.small = small;
     A.thr = d_thresholds; A.counts = d_counts; A.dist = d_dist;
     A.N = N;
+    A.early_exit = (early_exit && d_thresholds && !d_dist) ? 1 : 0;
     int stride = 128;                                    // power of two >= P (XOR swizzle needs >= 128)
     while (stride < P) stride <<= 1;
     A.plane_bytes = stride;

@@ -45,7 +45,7 @@ cudaError_t launch_crss_pairs(const uint16_t *d_needles, int64_t nn, const uint1
 cudaError_t launch_crss_search_tiles(const uint16_t *d_needles, int64_t nn,
                                      const uint16_t *d_haystack, int64_t nh, int N,
                                      const uint64_t *d_thresholds, uint32_t *d_counts,
-                                     uint64_t *d_dist, cudaStream_t s);
+                                     uint64_t *d_dist, cudaStream_t s, bool early_exit = false);
 
 // a9-a12 on the tensor cores (N = 64): rank counts with the int8 tcgen05 GEMM formulation,
 // exact fallback to the SIMT kernel for images outside the int8 guard.

@@ -1,0 +1,39 @@
+"""Clutterbox harness: histogram logic on CPU with the oracle injected as
+the compute, and the real CUDA path on the GPU."""
+import numpy as np
+import pytest
+
+from paper_2007_02306_b200.clutterbox import rank_histogram, run_scene
+
+
+def test_rank_histogram():
+    h = rank_histogram(np.array([0, 0, 3, 1, 0]), 10)
+    assert h["counts"] == {0: 3, 1: 1, 3: 1} and h["total"] == 5 and h["rank0_fraction"] == 0.6
+    with pytest.raises(ValueError):
+        rank_histogram(np.array([10]), 10)          # ranks live in [0, |CD|-1]
+
+
+def test_scene_protocol_with_oracle(oracle_mod):
+    """Level 1 = the reference alone: {CD} == {RD}, every self-distance is 0, so every rank is
+    exactly 0 (SPEC AC7, exact self-match).  With clutter, histogram totals = |RD|."""
+    R, N = 0.3, 64
+
+    def generate(mesh, origins):
+        return oracle_mod.rici_generate(mesh.vertices, mesh.indices, origins, R, N)["images"]
+
+    def search(needles, haystack):
+        return oracle_mod.ranks(needles, haystack)
+
+    out = run_scene(0, [1, 3], grid=(24, 12), generate=generate, search=search)
+    l1, l3 = out["levels"][1], out["levels"][3]
+    assert l1["rank0_fraction"] == 1.0 and l1["total"] == out["n_reference_vertices"]
+    assert l3["total"] == out["n_reference_vertices"] and l3["n_scene_vertices"] == 3 * 24 * 12
+    assert sum(l3["counts"].values()) == l3["total"]
+
+
+@pytest.mark.gpu
+def test_scene_protocol_cuda():
+    out = run_scene(1, [1, 4], grid=(64, 32))
+    assert out["levels"][1]["rank0_fraction"] == 1.0
+    assert 0.0 <= out["levels"][4]["rank0_fraction"] <= 1.0
+    assert out["levels"][4]["total"] == 64 * 32

@@ -284,3 +284,32 @@ def test_crss_paths_agree_subprocess(tmp_path):
         subprocess.run([sys.executable, "-c", code, f], env=env, check=True, timeout=600)
         outs[path] = np.load(f)
     assert np.array_equal(outs["simt"], outs["mma"])
+
+
+def _mini_c4(n_clutter=4, grid=(60, 30)):
+    """C4-shaped: needles = a reference object alone, haystack = the cluttered scene with the
+    reference placed first (so thresholds t_i > 0 and ranks are informative)."""
+    objs = [synth.bumpy_torus(grid[0], grid[1], key=(41, k), minor=0.25 + 0.05 * k, amp=0.08)
+            for k in range(1 + n_clutter)]
+    sc = synth.clutterbox(objs, key=(41, 1000))
+    n_ref = objs[0].n_vertices
+    ref = synth.Mesh(sc.vertices[:n_ref].copy(), objs[0].indices.copy(), sc.normals[:n_ref].copy())
+    return ref, sc
+
+
+def test_rank_modes_identical_c4_shaped(rici, oracle_mod):
+    """Full mode on the tensor cores, full mode on the SIMT path and rank mode with early exit
+     give identical ranks; a sample is checked against the oracle."""
+    ref, sc = _mini_c4()
+    nd = _dev(_gen(rici, ref, ref.origins, 0.3, 64))
+    hd = _dev(_gen(rici, sc, sc.origins, 0.3, 64))
+    r_mma = rici.rici_crss_search(nd, hd).cpu().numpy()
+    r_simt = rici.rici_crss_search(nd, hd, simt=True).cpu().numpy()
+    r_early = rici.rici_crss_search(nd, hd, early_exit=True).cpu().numpy()
+    assert np.array_equal(r_mma, r_simt) and np.array_equal(r_mma, r_early)
+    assert r_mma.max() > 0                                  # clutter makes some ranks non-zero
+    n = nd.cpu().numpy().view(np.uint16)
+    h = hd.cpu().numpy().view(np.uint16)
+    idx = np.random.default_rng(2).choice(n.shape[0], 48, replace=False)
+    thr = np.array([oracle_mod.crss(n[i], h[i]) for i in idx], np.uint64)
+    assert np.array_equal(r_mma[idx].astype(np.uint32), oracle_mod.count_below(n[idx], h, thr))
