@@ -313,3 +313,37 @@ def test_rank_modes_identical_c4_shaped(rici, oracle_mod):
     idx = np.random.default_rng(2).choice(n.shape[0], 48, replace=False)
     thr = np.array([oracle_mod.crss(n[i], h[i]) for i in idx], np.uint64)
     assert np.array_equal(r_mma[idx].astype(np.uint32), oracle_mod.count_below(n[idx], h, thr))
+
+
+@pytest.mark.slow
+def test_c3_clutterbox_full_size_sampled(rici, oracle_mod):
+    """C3 (BASELINE configs[2]): 10 objects, 998,560 triangles, RICI at all 499,280 scene
+    vertices on the GPU; the oracle checks a sample (incl. the last image) under the parity rule."""
+    cfg = synth.config_c3()
+    m = cfg["mesh"]
+    assert m.n_triangles == 998_560 and m.n_vertices == 499_280
+    g = _gen(rici, m, cfg["origins"], cfg["R"], cfg["N"])
+    idx = np.sort(np.random.default_rng(3).choice(m.n_vertices, 96, replace=False))
+    idx[-1] = m.n_vertices - 1
+    ref = oracle_mod.rici_generate(m.vertices, m.indices, cfg["origins"][idx], cfg["R"], cfg["N"], fragile=True)
+    _assert_parity(g[idx], ref)
+
+
+@pytest.mark.slow
+def test_c4_full_size_ranks_sampled(rici, oracle_mod):
+    """C4 (BASELINE configs[3]): 100,352 needles (reference alone) x 1,003,520 haystack images
+    (reference placed first + 9 clutter objects) ranked on the tensor cores; the oracle recounts
+    a sample of needles against the full haystack (bit-exact)."""
+    cfg = synth.config_c4()
+    ref, sc = cfg["reference"], cfg["scene"]
+    assert ref.n_vertices == 100_352 and sc.n_vertices == 1_003_520
+    nd = _dev(_gen(rici, ref, ref.origins, cfg["R"], cfg["N"]))
+    hm = rici.rici_create_mesh(torch.from_numpy(sc.vertices).to(DEV), torch.from_numpy(sc.indices).to(DEV))
+    hd = rici.rici_generate(hm, torch.from_numpy(sc.origins).to(DEV), cfg["R"], cfg["N"])
+    ranks = rici.rici_crss_search(nd, hd).cpu().numpy()
+    assert ranks.shape == (100_352,) and (ranks >= 0).all() and (ranks < 1_003_520).all()
+    idx = np.random.default_rng(4).choice(100_352, 8, replace=False)
+    n = nd.cpu().numpy().view(np.uint16)
+    h = hd.cpu().numpy().view(np.uint16)
+    thr = np.array([oracle_mod.crss(n[i], h[i]) for i in idx], np.uint64)
+    assert np.array_equal(ranks[idx].astype(np.uint32), oracle_mod.count_below(n[idx], h, thr))
