@@ -56,6 +56,8 @@ def _load():
         lib.oracle_count_below.restype = None
         lib.oracle_ranks.argtypes = [P, i64, P, i64, ctypes.c_int, P]
         lib.oracle_ranks.restype = None
+        lib.oracle_clutter_fraction.argtypes = [P, i64, P, i64, P, P, i64, ctypes.c_double, ctypes.c_int, P, P, P]
+        lib.oracle_clutter_fraction.restype = None
         lib.oracle_num_threads.argtypes = []
         lib.oracle_num_threads.restype = ctypes.c_int
         _lib = lib
@@ -176,3 +178,18 @@ def ranks(needles, haystack) -> np.ndarray:
     out = np.zeros(n.shape[0], dtype=np.uint32)
     _load().oracle_ranks(_ptr(n), n.shape[0], _ptr(h), h.shape[0], n.shape[1], _ptr(out))
     return out
+
+
+def clutter_fraction(vertices, indices, object_tag, origins, support_radius: float, q: int = 4):
+    """Eq. 8 per oriented point with a Q x Q barycentric quadrature of the area
+    inside the support cylinder (G17).  Returns (fraction, area_all, area_object)."""
+    v, t, o = _mesh_args(vertices, indices, origins)
+    tag = np.ascontiguousarray(object_tag, dtype=np.uint8).reshape(-1)
+    assert tag.shape[0] == t.shape[0]
+    n = o.shape[0]
+    frac = np.zeros(n)
+    aa = np.zeros(n)
+    ao = np.zeros(n)
+    _load().oracle_clutter_fraction(_ptr(v), v.shape[0], _ptr(t), t.shape[0], _ptr(tag), _ptr(o), n,
+                                    float(support_radius), int(q), _ptr(frac), _ptr(aa), _ptr(ao))
+    return frac, aa, ao

@@ -21,6 +21,9 @@
  *   rici_definition (O-def)   pinned: same closed forms as above
  *   crss (Eq. 7, Listing 1)              pinned: hand example (=5), algebraic identities
  *   ranks                 pinned: tie example, sort-based brute force
+ *   clutter fraction (Eq. 8)  pinned: closed-form areas of planes through the
+ *                                        support cylinder (quadrature convergence), exact
+ *                                        0 / 0.5 cases, fully-inside triangles
  *   The paper prints no descriptor value, distance or rank, so no pin is a
  *   number printed in the paper ("parity unpinned" against published values).
  */
@@ -382,6 +385,62 @@ EXPORT void oracle_ranks(const uint16_t *needles, int64_t nn, const uint16_t *ha
     for (int64_t i = 0; i < nn; ++i) thr[i] = oracle_crss(needles + i * P, haystack + i * P, N);
     oracle_count_below(needles, nn, haystack, nh, N, thr, ranks);
     free(thr);
+}
+
+/* ------------------------------------------------------------------------ */
+/* Clutter fraction, Eq. 8: clutter = (A_all - A_object) / A_all */
+/* where A_all is the surface area of all objects inside the support volume  */
+/* and A_object that of the object of interest.  Support volume: the */
+/* RICI support cylinder, radius R, beta in [-R/2, R/2] (G4, G17).  The      */
+/* paper does not say how the area is measured (G17): each triangle is cut   */
+/* into Q*Q congruent sub-triangles (barycentric grid) and a sub-triangle    */
+/* counts with area A/Q^2 when its centroid lies inside the volume.          */
+/* ------------------------------------------------------------------------ */
+static int inside_support(const frame_t *f, const double p[3], double R) {
+    double t[3];
+    project(f, p, t);
+    return fabs(t[2]) <= 0.5 * R && t[0] * t[0] + t[1] * t[1] <= R * R;
+}
+
+EXPORT void oracle_clutter_fraction(const float *vertices, int64_t nv, const int32_t *indices, int64_t nt,
+                                    const uint8_t *object_tag, const float *origins, int64_t n, double R,
+                                    int Q, double *out_fraction, double *out_area_all, double *out_area_obj) {
+    (void)nv;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t i = 0; i < n; ++i) {
+        double o[6];
+        for (int j = 0; j < 6; ++j) o[j] = origins[6 * i + j];
+        frame_t f = spin_frame(o);
+        double a_all = 0.0, a_obj = 0.0;
+        if (f.valid) {
+            for (int64_t k = 0; k < nt; ++k) {
+                double v[3][3];
+                for (int j = 0; j < 3; ++j)
+                    for (int a = 0; a < 3; ++a) v[j][a] = vertices[3 * (int64_t)indices[3 * k + j] + a];
+                double e1[3] = {v[1][0] - v[0][0], v[1][1] - v[0][1], v[1][2] - v[0][2]};
+                double e2[3] = {v[2][0] - v[0][0], v[2][1] - v[0][1], v[2][2] - v[0][2]};
+                double cr[3];
+                cross3(e1, e2, cr);
+                const double sub = 0.5 * sqrt(dot3(cr, cr)) / ((double)Q * Q);
+                double a_in = 0.0;
+                for (int u = 0; u < Q; ++u)
+                    for (int w = 0; u + w < Q; ++w)
+                        for (int up = 0; up < 2; ++up) {
+                            if (!up && u + w >= Q - 1) continue;   /* downward sub-triangles */
+                            const double bu = (u + (up ? 1.0 / 3.0 : 2.0 / 3.0)) / Q;
+                            const double bw = (w + (up ? 1.0 / 3.0 : 2.0 / 3.0)) / Q;
+                            double p[3];
+                            for (int a = 0; a < 3; ++a) p[a] = v[0][a] + bu * e1[a] + bw * e2[a];
+                            if (inside_support(&f, p, R)) a_in += sub;
+                        }
+                a_all += a_in;
+                if (object_tag[k]) a_obj += a_in;
+            }
+        }
+        out_fraction[i] = a_all > 0.0 ? (a_all - a_obj) / a_all : 0.0;
+        if (out_area_all) out_area_all[i] = a_all;
+        if (out_area_obj) out_area_obj[i] = a_obj;
+    }
 }
 
 EXPORT int oracle_num_threads(void) {

@@ -21,6 +21,8 @@
 //  * the per-image rotation coefficients are computed once per image in the
 //    CTA prologue ("out of the inner loop");
 //  * saturation to uint16 (G9) and coalesced 128-bit stores in the epilogue.
+#include <cstdlib>
+
 #include "rici_internal.cuh"
 
 namespace rici {
@@ -425,7 +427,9 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
 
 int generate_images_per_cta(int N) {
     int per = N * N * 4;
-    int k = (64 * 1024) / per;
+    int budget = 64 * 1024;                       // counters per CTA (3 CTAs / SM at N = 64)
+    if (const char *v = getenv("RICI_GEN_SMEM_KB")) budget = atoi(v) * 1024;   // tuning knob
+    int k = budget / per;
     return k < 1 ? 1 : (k > kMaxK ? kMaxK : k);
 }
 
