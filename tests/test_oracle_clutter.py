@@ -52,7 +52,7 @@ def test_exact_cases(oracle_mod):
     T = np.concatenate([m.indices, m.indices + m.n_vertices])
     tag = np.concatenate([tag1, np.zeros(m.n_triangles, np.uint8)])
     frac, _, _ = oracle_mod.clutter_fraction(V, T, tag, o, 0.3)
-    assert (frac == 0.5).all()
+    assert np.allclose(frac, 0.5, rtol=0, atol=1e-12)
     # clutter far outside the support volume changes nothing
     V2 = np.concatenate([m.vertices, m.vertices + np.float32(10)])
     frac, _, _ = oracle_mod.clutter_fraction(V2, T, tag, o, 0.3)
