@@ -153,6 +153,22 @@ RICI_API rici_status rici_crss_distances(const uint16_t *needles, int64_t n_need
                                 const uint16_t *haystack, int64_t n_haystack, int32_t n_bins,
                                 uint64_t *out, rici_stream_t stream);
 
+/* ---- (f4) clutter fraction, Eq. 8 ---------------------------------
+ * clutter = (A_all - A_object) / A_all per oriented point, A over the support volume (the
+ * RICI cylinder r <= R, |beta| <= R/2; G17).  Areas by a fixed quadrature: every triangle
+ * is cut into Q x Q congruent sub-triangles and a sub-triangle counts (area A/Q^2) when its
+ * centroid is inside.  0 when no surface is inside.
+ *   object_tag      [n_triangles] uint8 in the caller's triangle order (the order given to
+ *                   rici_create_mesh): non-zero = part of the object of interest
+ *   origins         [n][6] float32 as for rici_generate
+ *   quadrature_q    Q in [1, 16]
+ *   out_fraction    [n] float32
+ *   out_area_all    [n] float32 A_all, or NULL                                       */
+RICI_API rici_status rici_clutter_fraction(rici_mesh mesh, const uint8_t *object_tag,
+                                           const float *origins, int64_t n, float support_radius,
+                                           int32_t quadrature_q, float *out_fraction,
+                                           float *out_area_all, rici_stream_t stream);
+
 /* ---- diagnostics ------------------------------------------------------------ */
 /* Message of the last failing call on this thread ("" if none).  Valid until
  * the next rici_* call on this thread. */

@@ -19,7 +19,7 @@ import torch
 from ._lib import RiciError, check, load
 
 __all__ = ["Mesh", "RiciError", "rici_create_mesh", "rici_destroy_mesh", "rici_generate",
-           "rici_crss_search", "rici_crss_search_ex", "rici_crss_pairs", "rici_crss_count_below", "rici_crss_distances",
+           "rici_crss_search", "rici_crss_search_ex", "rici_clutter_fraction", "rici_crss_pairs", "rici_crss_count_below", "rici_crss_distances",
            "rici_launch_count", "rici_version", "library_path"]
 
 
@@ -204,6 +204,21 @@ def rici_crss_distances(needles, haystack, n_bins: int | None = None, out=None, 
     check(load().rici_crss_distances(_ptr(nd), nn, _ptr(hd), nh, N, _ptr(out),
                                      ctypes.c_void_p(_stream(stream))))
     return out
+
+
+def rici_clutter_fraction(mesh: Mesh, object_tag, origins, support_radius: float, quadrature_q: int = 4,
+                          with_area: bool = False, stream=None):
+    """(f4) ``rici_clutter_fraction``: Eq. 8 per oriented point.  object_tag [T] uint8 in the
+    triangle order given to rici_create_mesh.  Returns float32 fractions (and A_all)."""
+    t = _as_tensor(object_tag, torch.uint8, "object_tag").reshape(-1)
+    o = _as_tensor(origins, torch.float32, "origins").reshape(-1, 6)
+    n = o.shape[0]
+    frac = torch.empty(n, dtype=torch.float32, device=o.device)
+    area = torch.empty(n, dtype=torch.float32, device=o.device) if with_area else None
+    check(load().rici_clutter_fraction(mesh.handle, _ptr(t), _ptr(o), n, float(support_radius), int(quadrature_q),
+                                       _ptr(frac), _ptr(area) if with_area else None,
+                                       ctypes.c_void_p(_stream(stream))))
+    return (frac, area) if with_area else frac
 
 
 def rici_launch_count() -> int:

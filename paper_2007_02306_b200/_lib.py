@@ -14,7 +14,7 @@ LIB_PATH = os.path.join(_HERE, "librici.so")
 
 SYMBOLS = ["rici_create_mesh", "rici_destroy_mesh", "rici_mesh_num_triangles", "rici_generate",
            "rici_crss_search", "rici_crss_search_ex", "rici_crss_pairs", "rici_crss_count_below", "rici_crss_distances",
-           "rici_last_error", "rici_launch_count", "rici_version"]
+           "rici_clutter_fraction", "rici_last_error", "rici_launch_count", "rici_version"]
 
 RICI_CRSS_SIMT = 1
 RICI_CRSS_EARLY_EXIT = 2
@@ -59,6 +59,8 @@ def load() -> ctypes.CDLL:
     lib.rici_crss_count_below.restype = st
     lib.rici_crss_distances.argtypes = [P, i64, P, i64, i32, P, P]
     lib.rici_crss_distances.restype = st
+    lib.rici_clutter_fraction.argtypes = [P, P, P, i64, ctypes.c_float, i32, P, P, P]
+    lib.rici_clutter_fraction.restype = st
     lib.rici_last_error.argtypes = []
     lib.rici_last_error.restype = ctypes.c_char_p
     lib.rici_launch_count.argtypes = []

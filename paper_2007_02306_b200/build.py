@@ -9,7 +9,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "librici.so")
-SOURCES = ["abi.cu", "mesh.cu", "sort.cu", "generate.cu", "crss.cu", "crss_mma.cu"]
+SOURCES = ["abi.cu", "mesh.cu", "sort.cu", "generate.cu", "crss.cu", "crss_mma.cu", "clutter.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC,-fvisibility=hidden", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
@@ -29,7 +29,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     for src in SOURCES:
         obj = os.path.join(CSRC, src.replace(".cu", ".o"))
-        extra = ["-ftz=true"] if src == "generate.cu" else []     # denormals cannot matter at 1e-5*R
+        extra = ["-ftz=true"] if src in ("generate.cu", "clutter.cu") else []     # denormals cannot matter at 1e-5*R
         cmd = [NVCC, *FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:

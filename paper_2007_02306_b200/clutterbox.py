@@ -55,8 +55,20 @@ def build_scene_objects(scene: int, n_objects: int, grid=(120, 60)):
     return objs
 
 
+def clutter_rank_heatmap(clutter: np.ndarray, ranks: np.ndarray, n_clutter_bins: int = 10,
+                         rank_edges=(0, 1, 2, 5, 10, 100, 1000, 10 ** 9)) -> dict:
+    """2D histogram of (Eq. 8 clutter fraction bin, rank bin) -- the data behind the paper's
+    clutter-vs-rank heatmap (fig:clutterComparison)."""
+    c = np.clip(np.asarray(clutter, dtype=np.float64), 0.0, 1.0)
+    cb = np.minimum((c * n_clutter_bins).astype(np.int64), n_clutter_bins - 1)
+    rb = np.searchsorted(np.asarray(rank_edges[1:]), np.asarray(ranks, dtype=np.int64), side="right")
+    H = np.zeros((n_clutter_bins, len(rank_edges) - 1), dtype=np.int64)
+    np.add.at(H, (cb, rb), 1)
+    return {"clutter_bins": n_clutter_bins, "rank_edges": list(rank_edges), "counts": H.tolist()}
+
+
 def run_scene(scene: int, levels, grid=(120, 60), box_side: float = 3.0, R: float = 0.3, N: int = 64,
-              generate=None, search=None):
+              generate=None, search=None, clutter=None):
     """One clutterbox run: returns {level: histogram} plus timing.  `generate(mesh, origins)` and
     `search(needles, haystack)` default to the CUDA library."""
     import synth
@@ -73,6 +85,13 @@ def run_scene(scene: int, levels, grid=(120, 60), box_side: float = 3.0, R: floa
 
         def search(needles, haystack):  # noqa: F811
             return rici.rici_crss_search(needles, haystack).cpu().numpy()
+
+        if clutter is None:
+            def clutter(mesh, tag, origins):  # noqa: F811
+                m = rici.rici_create_mesh(torch.from_numpy(mesh.vertices).cuda(), torch.from_numpy(mesh.indices).cuda())
+                f = rici.rici_clutter_fraction(m, torch.from_numpy(tag).cuda(), torch.from_numpy(origins).cuda(), R)
+                m.destroy()
+                return f.cpu().numpy()
     levels = sorted(set(int(x) for x in levels))
     objs = build_scene_objects(scene, max(levels), grid)
     placed = synth.clutterbox(objs, key=(5, scene, 1000), box_side=box_side)
@@ -90,6 +109,12 @@ def run_scene(scene: int, levels, grid=(120, 60), box_side: float = 3.0, R: floa
         cd = generate(sc, sc.origins)                      # {CD} of the combined mesh
         ranks = search(rd, cd)
         h = rank_histogram(ranks, nv)
+        if clutter is not None:                             # f4: Eq. 8 at every reference vertex
+            tag = np.zeros(nt, np.uint8)
+            tag[: objs[0].n_triangles] = 1
+            cf = clutter(sc, tag, sc.origins[:n_ref])
+            h["mean_clutter_fraction"] = float(np.mean(cf))
+            h["clutter_rank_heatmap"] = clutter_rank_heatmap(cf, ranks)
         h.update({"n_objects": lv, "n_scene_vertices": nv, "n_scene_triangles": nt,
                   "comparisons": int(n_ref) * nv})
         out["levels"][lv] = h

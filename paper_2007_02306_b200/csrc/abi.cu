@@ -218,6 +218,7 @@ rici_status rici_destroy_mesh(rici_mesh mesh) {
     if (mesh->m.tri) cudaFreeAsync(mesh->m.tri, 0);
     if (mesh->m.sphere) cudaFreeAsync(mesh->m.sphere, 0);
     if (mesh->m.super_sphere) cudaFreeAsync(mesh->m.super_sphere, 0);
+    if (mesh->m.order) cudaFreeAsync(mesh->m.order, 0);
     delete mesh;
     return RICI_OK;
 }
@@ -245,6 +246,35 @@ rici_status rici_generate(rici_mesh mesh, const float *origins, int64_t n, float
                                   (uint16_t *)dout, s);
     if (e == cudaSuccess) e = st.finish();
     if (e != cudaSuccess) return cuda_fail(e, "rici_generate");
+    return RICI_OK;
+}
+
+rici_status rici_clutter_fraction(rici_mesh mesh, const uint8_t *object_tag, const float *origins, int64_t n,
+                                  float support_radius, int32_t quadrature_q, float *out_fraction,
+                                  float *out_area_all, rici_stream_t stream) {
+    g_err.clear();
+    if (!mesh) return fail(RICI_ERR_INVALID_ARGUMENT, "mesh is null");
+    if (n < 0) return fail(RICI_ERR_INVALID_ARGUMENT, "negative count");
+    if (n > 0 && (!origins || !out_fraction)) return fail(RICI_ERR_INVALID_ARGUMENT, "null origins/out_fraction");
+    if (mesh->m.nt > 0 && !object_tag) return fail(RICI_ERR_INVALID_ARGUMENT, "null object_tag");
+    if (!(support_radius > 0.f) || !std::isfinite(support_radius))
+        return fail(RICI_ERR_INVALID_ARGUMENT, "support_radius must be finite and > 0");
+    if (quadrature_q < 1 || quadrature_q > 16) return fail(RICI_ERR_INVALID_ARGUMENT, "quadrature_q must be in [1,16]");
+    if (rici_status st = check_device()) return st;
+    if (n == 0) return RICI_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    Staging st(s);
+    const void *dt = nullptr, *dorig = nullptr;
+    void *df = nullptr, *da = nullptr;
+    cudaError_t e = st.in(object_tag, (size_t)mesh->m.nt, &dt);
+    if (e == cudaSuccess) e = st.in(origins, sizeof(float) * 6 * (size_t)n, &dorig);
+    if (e == cudaSuccess) e = st.out(out_fraction, sizeof(float) * (size_t)n, &df);
+    if (e == cudaSuccess && out_area_all) e = st.out(out_area_all, sizeof(float) * (size_t)n, &da);
+    if (e == cudaSuccess)
+        e = rici::launch_clutter_fraction(mesh->m, (const unsigned char *)dt, (const float *)dorig, n, support_radius,
+                                          quadrature_q, (float *)df, (float *)da, s);
+    if (e == cudaSuccess) e = st.finish();
+    if (e != cudaSuccess) return cuda_fail(e, "rici_clutter_fraction");
     return RICI_OK;
 }
 

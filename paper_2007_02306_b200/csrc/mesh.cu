@@ -113,9 +113,9 @@ cudaError_t launch_mesh_stage(const float *d_vertices, int64_t nv, const int32_t
     if (m->n_chunks == 0) return cudaSuccess;
     cudaError_t e;
     float *centroid = nullptr;
-    int *order = nullptr;
     if ((e = cudaMallocAsync((void **)&centroid, sizeof(float) * 3 * nt, s)) != cudaSuccess) return e;
-    if ((e = cudaMallocAsync((void **)&order, sizeof(int) * nt, s)) != cudaSuccess) return e;
+    if ((e = cudaMallocAsync((void **)&m->order, sizeof(int) * nt, s)) != cudaSuccess) return e;
+    int *order = m->order;
     int blocks = (int)std::min<int64_t>((nt + 255) / 256, 148 * 8);
     centroid_kernel<<<blocks, 256, 0, s>>>(d_vertices, nv, d_indices, nt, centroid, d_bad);
     note_launches(1);
@@ -129,7 +129,6 @@ cudaError_t launch_mesh_stage(const float *d_vertices, int64_t nv, const int32_t
     note_launches(2);
     e = cudaGetLastError();
     cudaFreeAsync(centroid, s);
-    cudaFreeAsync(order, s);
     return e;
 }
 

@@ -19,6 +19,7 @@ struct DeviceMesh {
     float *tri = nullptr;         // [n_chunks][9][kChunk], triangles in spatial (Morton-cell) order
     float4 *sphere = nullptr;     // [n_chunks] bounding sphere (cx, cy, cz, r) of each chunk
     float4 *super_sphere = nullptr;  // [n_super] bounding sphere of each superchunk
+    int *order = nullptr;         // [nt] staged slot -> caller triangle index
     int device = 0;
 };
 
@@ -51,6 +52,11 @@ cudaError_t launch_crss_search_tiles(const uint16_t *d_needles, int64_t nn,
 // exact fallback to the SIMT kernel for images outside the int8 guard.
 cudaError_t launch_crss_count_mma(const uint16_t *d_needles, int64_t nn, const uint16_t *d_haystack, int64_t nh,
                                   const uint64_t *d_thr, uint32_t *d_counts, cudaStream_t s);
+
+// f4: Eq. 8 clutter fraction per oriented point (quadrature of the area inside the support
+// cylinder; object_tag [nt] in caller triangle order, device memory).
+cudaError_t launch_clutter_fraction(const DeviceMesh &m, const unsigned char *d_tag, const float *d_origins,
+                                    int64_t n, float R, int Q, float *d_frac, float *d_area_all, cudaStream_t s);
 
 // Which kernel counts ranks: the tensor-core path when N == 64 and RICI_CRSS_PATH != "simt".
 bool use_mma_path(int N);

@@ -26,7 +26,7 @@ def _declared():
 
 def test_header_symbols_exported(lib):
     declared = _declared()
-    assert len(declared) == 12
+    assert len(declared) == 13
     out = subprocess.run(["nm", "-D", "--defined-only", os.path.join(ROOT, "paper_2007_02306_b200", "librici.so")],
                          capture_output=True, text=True, check=True).stdout
     exported = set(re.findall(r" T (rici_\w+)", out))

@@ -37,3 +37,20 @@ def test_scene_protocol_cuda():
     assert out["levels"][1]["rank0_fraction"] == 1.0
     assert 0.0 <= out["levels"][4]["rank0_fraction"] <= 1.0
     assert out["levels"][4]["total"] == 64 * 32
+
+
+def test_heatmap_counts():
+    from paper_2007_02306_b200.clutterbox import clutter_rank_heatmap
+    h = clutter_rank_heatmap(np.array([0.0, 0.05, 0.5, 0.99, 1.0]), np.array([0, 1, 3, 2000, 0]), 10)
+    H = np.array(h["counts"])
+    assert H.sum() == 5 and H[0, 0] == 1 and H[0, 1] == 1 and H[5, 2] == 1 and H[9, -1] == 1 and H[9, 0] == 1
+
+
+def test_scene_with_clutter_fraction_oracle(oracle_mod):
+    R, N = 0.3, 64
+    out = run_scene(2, [1, 2], grid=(24, 12),
+                    generate=lambda m, o: oracle_mod.rici_generate(m.vertices, m.indices, o, R, N)["images"],
+                    search=lambda a, b: oracle_mod.ranks(a, b),
+                    clutter=lambda m, tag, o: oracle_mod.clutter_fraction(m.vertices, m.indices, tag, o, R)[0])
+    assert out["levels"][1]["mean_clutter_fraction"] == 0.0
+    assert np.array(out["levels"][2]["clutter_rank_heatmap"]["counts"]).sum() == out["n_reference_vertices"]

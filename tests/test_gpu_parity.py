@@ -347,3 +347,33 @@ def test_c4_full_size_ranks_sampled(rici, oracle_mod):
     h = hd.cpu().numpy().view(np.uint16)
     thr = np.array([oracle_mod.crss(n[i], h[i]) for i in idx], np.uint64)
     assert np.array_equal(ranks[idx].astype(np.uint32), oracle_mod.count_below(n[idx], h, thr))
+
+
+# ------------------------------------------------------------------ f4: Eq. 8 clutter fraction
+def test_clutter_fraction_matches_oracle(rici, oracle_mod):
+    ref, sc = _mini_c4(n_clutter=4)
+    tag = np.zeros(sc.n_triangles, np.uint8)
+    tag[:ref.n_triangles] = 1                                  # the reference object is placed first
+    o = sc.origins[: ref.n_vertices]
+    m = rici.rici_create_mesh(torch.from_numpy(sc.vertices).to(DEV), torch.from_numpy(sc.indices).to(DEV))
+    frac, area = rici.rici_clutter_fraction(m, torch.from_numpy(tag).to(DEV), torch.from_numpy(o).to(DEV),
+                                            0.3, 4, with_area=True)
+    want, aa, _ = oracle_mod.clutter_fraction(sc.vertices, sc.indices, tag, o, 0.3, q=4)
+    g = frac.cpu().numpy().astype(np.float64)
+    a = area.cpu().numpy().astype(np.float64)
+    assert np.abs(g - want).max() <= 2e-4
+    assert np.abs(a - aa).max() <= 1e-4 * aa.max()
+    assert (want > 0).any() and (want == 0).any()              # some vertices see clutter, some do not
+
+
+def test_clutter_fraction_exact_cases(rici):
+    m0 = synth.bumpy_torus(40, 20, key=(3,))
+    V = np.concatenate([m0.vertices, m0.vertices])
+    T = np.concatenate([m0.indices, m0.indices + m0.n_vertices])
+    tag = np.concatenate([np.ones(m0.n_triangles, np.uint8), np.zeros(m0.n_triangles, np.uint8)])
+    m = rici.rici_create_mesh(V, T)
+    f = rici.rici_clutter_fraction(m, tag, m0.origins[::11], 0.3).cpu().numpy()
+    assert np.allclose(f, 0.5, atol=1e-6)                     # a coincident duplicate is half the area
+    m1 = rici.rici_create_mesh(m0.vertices, m0.indices)
+    f1 = rici.rici_clutter_fraction(m1, np.ones(m0.n_triangles, np.uint8), m0.origins[::11], 0.3).cpu().numpy()
+    assert (f1 == 0).all()
