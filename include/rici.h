@@ -69,7 +69,8 @@ typedef enum {
  *   vertices   [n_vertices][3] float32 x,y,z
  *   indices    [n_triangles][3] int32, each in [0, n_vertices)
  *   out_mesh   receives the handle (unchanged on error)
- * n_triangles = 0 is a valid empty scene (every image is zero).
+ * n_triangles = 0 is a valid empty scene (every image is zero); at most 268,435,456
+ * triangles (RICI_ERR_INVALID_ARGUMENT beyond).
  * Index validation reads the indices, so this call synchronises `stream`;
  * an out-of-range index returns RICI_ERR_INVALID_ARGUMENT.                   */
 RICI_API rici_status rici_create_mesh(const float *vertices, int64_t n_vertices,

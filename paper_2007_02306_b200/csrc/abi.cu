@@ -7,6 +7,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -20,6 +22,20 @@ struct rici_mesh_s {
 namespace rici {
 static std::atomic<unsigned long long> g_launches{0};
 void note_launches(int k) { g_launches.fetch_add((unsigned long long)k, std::memory_order_relaxed); }
+cudaError_t ensure_smem(const void *kernel, size_t bytes) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    static std::mutex mu;
+    static std::map<std::pair<const void *, int>, size_t> done;
+    std::lock_guard<std::mutex> lock(mu);
+    auto key = std::make_pair(kernel, dev);
+    auto it = done.find(key);
+    if (it != done.end() && it->second >= bytes) return cudaSuccess;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) done[key] = bytes;
+    return e;
+}
 bool use_mma_path(int N) {
     static int mode = -1;                  // 1 = tensor cores where applicable, 0 = SIMT only
     if (mode < 0) {
@@ -52,32 +68,36 @@ rici_status cuda_fail(cudaError_t e, const char *what) {
     return fail(RICI_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
 }
 
-// sm_100 only (the kernels are compiled for sm_100a and nothing else).
+// sm_100 only (the kernels are compiled for sm_100a and nothing else).  Per-device result and
+// pool setting are cached under a mutex (the ABI may be called from several host threads).
 rici_status check_device() {
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
-    static int cached[64];
-    static bool init = false;
-    if (!init) { for (int &c : cached) c = -1; init = true; }
-    if (dev >= 0 && dev < 64 && cached[dev] >= 0)
-        return cached[dev] ? RICI_OK : fail(RICI_ERR_UNSUPPORTED, "device %d is not sm_100", dev);
-    int major = 0, minor = 0;
-    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
-    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
-    bool ok = (major == 10 && minor == 0);
-    if (dev >= 0 && dev < 64) cached[dev] = ok ? 1 : 0;
-    if (!ok) return fail(RICI_ERR_UNSUPPORTED, "device %d is sm_%d%d; this build is sm_100a only", dev, major, minor);
-    // keep freed workspace in the stream-ordered pool between calls
-    static bool pool_set[64] = {};
-    if (dev < 64 && !pool_set[dev]) {
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t thr = ~0ull;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    static std::mutex mu;
+    static std::map<int, bool> ok_dev;
+    bool ok;
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        auto it = ok_dev.find(dev);
+        if (it == ok_dev.end()) {
+            int major = 0, minor = 0;
+            cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+            cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+            ok = (major == 10 && minor == 0);
+            if (ok) {                          // keep freed workspace in the stream-ordered pool
+                cudaMemPool_t pool;
+                if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                    uint64_t thr = ~0ull;
+                    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+                }
+            }
+            ok_dev[dev] = ok;
+        } else {
+            ok = it->second;
         }
-        pool_set[dev] = true;
     }
+    if (!ok) return fail(RICI_ERR_UNSUPPORTED, "device %d is not sm_100; this build is sm_100a only", dev);
     return RICI_OK;
 }
 
@@ -167,6 +187,8 @@ rici_status rici_create_mesh(const float *vertices, int64_t n_vertices, const in
         return fail(RICI_ERR_INVALID_ARGUMENT, "null vertices/indices");
     if (n_triangles > 0 && n_vertices == 0)
         return fail(RICI_ERR_INVALID_ARGUMENT, "triangles given but no vertices");
+    if (n_triangles > rici::kMaxTriangles)
+        return fail(RICI_ERR_INVALID_ARGUMENT, "at most %lld triangles per mesh", (long long)rici::kMaxTriangles);
     if (rici_status st = check_device()) return st;
     cudaStream_t s = (cudaStream_t)stream;
     rici_mesh_s *mesh = new (std::nothrow) rici_mesh_s();

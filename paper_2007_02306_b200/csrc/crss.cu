@@ -533,12 +533,7 @@ cudaError_t launch_crss_search_tiles(const uint16_t *d_needles, int64_t nn,
     A.n_groups = (A.n_tiles + A.tiles_per_group - 1) / A.tiles_per_group;
     A.n_items = n_chunks * A.n_groups;
     A.work = work;
-    static size_t attr_smem = 0;                          // static + dynamic must stay <= 227 KB
-    if (smem > attr_smem) {
-        e = cudaFuncSetAttribute(crss_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        attr_smem = smem;
-    }
+    if ((e = ensure_smem((const void *)crss_tile_kernel, smem)) != cudaSuccess) return e;
     int64_t grid = A.n_items < sms ? A.n_items : sms;
     crss_tile_kernel<<<(unsigned)grid, kCrssThreads, smem, s>>>(A);
     note_launches(1);

@@ -405,12 +405,9 @@ cudaError_t launch_generate(const DeviceMesh &m, const float *d_origins, int64_t
     if (n == 0) return cudaSuccess;
     const int K = generate_images_per_cta(N);
     size_t smem = (size_t)K * N * N * sizeof(int);
-    static size_t attr_smem = 0;
-    if (smem > attr_smem) {
-        cudaError_t e = cudaFuncSetAttribute(generate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
+    {
+        cudaError_t e = ensure_smem((const void *)generate_kernel, smem);
         if (e != cudaSuccess) return e;
-        attr_smem = smem;
     }
     // build the images in spatial order so a CTA's K support volumes are compact
     int *perm = nullptr;

@@ -29,6 +29,13 @@ cudaError_t spatial_order(const float *d_pts, int stride, int64_t n, int *d_perm
 // Kernel-launch bookkeeping (rici_launch_count()).
 void note_launches(int k);
 
+// Raises a kernel's dynamic shared-memory limit to `bytes` on the current device (once per
+// (kernel, device); thread-safe).
+cudaError_t ensure_smem(const void *kernel, size_t bytes);
+
+// Largest triangle count the construction work items can address (chunk index << 8 in 31 bits).
+constexpr int64_t kMaxTriangles = ((int64_t)1 << 23) * 32;
+
 // a1: de-index + chunk layout + chunk spheres; *d_bad set to 1 on an out-of-range index.
 cudaError_t launch_mesh_stage(const float *d_vertices, int64_t nv, const int32_t *d_indices,
                               int64_t nt, DeviceMesh *m, int *d_bad, cudaStream_t s);

@@ -53,6 +53,10 @@ def test_version_and_argument_validation(lib):
     assert lib.rici_crss_search(P(1), 6, P(1), 5, 64, P(1), None) == 1      # n_haystack < n_needles
     assert lib.rici_crss_pairs(P(1), 1, P(1), 1, 1, P(1), 1, P(1), None) == 1  # n_bins < 2
     assert lib.rici_crss_distances(P(1), 1, P(1), 1, 129, P(1), None) == 1    # n_bins > 128
+    assert lib.rici_create_mesh(P(1), 3, P(1), (1 << 28) + 1, None, ctypes.byref(h)) == 1   # > max triangles
+    assert b"triangles" in lib.rici_last_error()
+    assert lib.rici_crss_search_ex(P(1), 1, P(1), 1, 64, 8, P(1), None) == 1                 # unknown flag
+    assert lib.rici_clutter_fraction(None, None, None, 0, ctypes.c_float(0.3), 4, None, None, None) == 1
     assert lib.rici_destroy_mesh(None) == 0
     assert lib.rici_mesh_num_triangles(None) == -1
 

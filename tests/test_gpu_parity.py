@@ -377,3 +377,32 @@ def test_clutter_fraction_exact_cases(rici):
     m1 = rici.rici_create_mesh(m0.vertices, m0.indices)
     f1 = rici.rici_clutter_fraction(m1, np.ones(m0.n_triangles, np.uint8), m0.origins[::11], 0.3).cpu().numpy()
     assert (f1 == 0).all()
+
+
+def test_streams_and_threads(rici):
+    """Work enqueued on non-default streams, from two host threads at once, gives the same
+    images and ranks as the default stream (stream-ordered workspace, thread-safe ABI state)."""
+    import threading
+    cfg = synth.config_c1()
+    m = synth.bumpy_torus(80, 40, key=(17,))
+    ref = _gen(rici, m, m.origins, 0.3, 64)
+    ref_r = rici.rici_crss_search(_dev(ref), _dev(ref)).cpu().numpy()
+    out = {}
+
+    def work(tag):
+        st = torch.cuda.Stream()
+        with torch.cuda.stream(st):
+            mesh = rici.rici_create_mesh(torch.from_numpy(m.vertices).to(DEV), torch.from_numpy(m.indices).to(DEV),
+                                         stream=st)
+            im = rici.rici_generate(mesh, torch.from_numpy(m.origins).to(DEV), 0.3, 64, stream=st)
+            r = rici.rici_crss_search(im, im, stream=st)
+            st.synchronize()
+            out[tag] = (im.cpu().numpy().view(np.uint16), r.cpu().numpy())
+    th = [threading.Thread(target=work, args=(t,)) for t in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for t in range(2):
+        assert np.array_equal(out[t][0], ref) and np.array_equal(out[t][1], ref_r)
+    assert cfg["N"] == 64
