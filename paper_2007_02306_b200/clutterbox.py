@@ -122,24 +122,63 @@ def run_scene(scene: int, levels, grid=(120, 60), box_side: float = 3.0, R: floa
     return out
 
 
+def parse_levels(text: str):
+    """'1,5,10' or '1-20' (inclusive range) or a mix: '1-5,10,20'."""
+    out = []
+    for part in text.split(","):
+        if "-" in part:
+            a, b = part.split("-")
+            out += list(range(int(a), int(b) + 1))
+        else:
+            out.append(int(part))
+    return sorted(set(out))
+
+
 def main():
+    """C5 (BASELINE configs[4]): S scenes x clutter levels.  Under torchrun the scenes are split
+    over the ranks (independent problems, weak scaling); rank 0 gathers the histograms."""
     ap = argparse.ArgumentParser()
     ap.add_argument("--scenes", type=int, default=2)
     ap.add_argument("--levels", default="1,5,10")
     ap.add_argument("--grid", default="120,60", help="torus grid per object (nu,nv)")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
-    levels = [int(x) for x in a.levels.split(",")]
+    levels = parse_levels(a.levels)
     grid = tuple(int(x) for x in a.grid.split(","))
-    res = [run_scene(s, levels, grid) for s in range(a.scenes)]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        dist.init_process_group("nccl")
+    t0 = time.perf_counter()
+    res = [run_scene(sc, levels, grid) for sc in range(rank, a.scenes, world)]
+    wall = time.perf_counter() - t0
+    if world > 1:
+        gathered = [None] * world
+        dist.all_gather_object(gathered, (res, wall))
+        res = [r for part, _ in gathered for r in part]
+        wall = max(w for _, w in gathered)
+        dist.destroy_process_group()
+    if rank != 0:
+        return
+    res.sort(key=lambda r: r["scene"])
     summary = {lv: float(np.mean([r["levels"][lv]["rank0_fraction"] for r in res])) for lv in levels}
+    clutter = {lv: float(np.mean([r["levels"][lv].get("mean_clutter_fraction", 0.0) for r in res])) for lv in levels}
+    n_img = sum(r["levels"][lv]["n_scene_vertices"] for r in res for lv in levels) + sum(r["n_reference_vertices"] for r in res)
+    n_cmp = sum(r["levels"][lv]["comparisons"] for r in res for lv in levels)
     doc = {"protocol": "clutterbox (P:379-391), synthetic tori", "levels": levels, "grid": grid,
-           "mean_rank0_fraction": summary, "runs": res}
+           "scenes": a.scenes, "world_size": world, "wall_s": wall,
+           "images_generated": n_img, "comparisons": n_cmp,
+           "mean_rank0_fraction": summary, "mean_clutter_fraction": clutter, "runs": res}
     txt = json.dumps(doc, indent=1, default=str)
     if a.out:
         with open(a.out, "w") as f:
             f.write(txt)
-    print(json.dumps({"mean_rank0_fraction": summary, "seconds": sum(r["seconds"] for r in res)}))
+    print(json.dumps({"scenes": a.scenes, "levels": [levels[0], levels[-1]], "world_size": world, "wall_s": wall,
+                      "images_per_s": n_img / wall, "comparisons_per_s": n_cmp / wall,
+                      "mean_rank0_fraction": summary, "mean_clutter_fraction": clutter}))
 
 
 if __name__ == "__main__":
