@@ -406,3 +406,23 @@ def test_streams_and_threads(rici):
     for t in range(2):
         assert np.array_equal(out[t][0], ref) and np.array_equal(out[t][1], ref_r)
     assert cfg["N"] == 64
+
+
+def test_saturation_at_65535(rici, oracle_mod):
+    """G9: counts saturate at 65535.  33,000 copies of a vertical quad give 66,000 crossings per
+    pixel beyond rho = a; the int32 difference arrays stay exact and the store saturates.  The
+    saturated images also exercise CRSS's exact 64-bit path (pixels > 127)."""
+    q = synth.quad([[0.2, -5, -5], [0.2, 5, -5], [0.2, 5, 5], [0.2, -5, 5]])
+    reps = 33_000
+    V = np.tile(q.vertices, (reps, 1))
+    T = (q.indices[None, :, :] + 4 * np.arange(reps)[:, None, None]).reshape(-1, 3).astype(np.int32)
+    m = synth.Mesh(V, T, np.zeros_like(V))
+    o = np.array([[0, 0, 0, 0, 0, 1], [0.01, 0.02, 0.0, 0.1, 0.0, 1.0]], np.float32)
+    g = _gen(rici, m, o, 1.0, 64)
+    want = oracle_mod.rici_generate(V, T, o, 1.0, 64)["images"]
+    assert g.max() == 65535
+    assert np.array_equal(g, want)
+    d = rici.rici_crss_distances(_dev(g), _dev(g)).cpu().numpy().view(np.uint64)
+    assert np.array_equal(d, oracle_mod.crss_matrix(g, g))
+    r = rici.rici_crss_search(_dev(g), _dev(g)).cpu().numpy()
+    assert np.array_equal(r.astype(np.uint32), oracle_mod.ranks(g, g))
