@@ -89,22 +89,22 @@ __device__ __forceinline__ void rasterise_triangle(int *__restrict__ acc, const 
             float u = (beta - bz) * inv_bc;
             e1x = fmaf(u, cx - bx, bx); e1y = fmaf(u, cy - by, by);
         }
-        // Step 2: rotate so E0E1 is parallel to x; the normalised direction is (cos, sin).
-        float dx = e1x - e0x, dy = e1y - e0y;
-        float l2 = dx * dx + dy * dy;
+        // Step 2: rotate so E0E1 is parallel to x with the normalised direction D/|D| as
+        // (cos, sin): the rotated x of E0 / E1 is (D.E0)/|D| / (D.E1)/|D|, so their signs are
+        // those of D.E0 and D.E0 + |D|^2 -- the normalisation is only needed for |C| below.
+        const float dx = e1x - e0x, dy = e1y - e0y;
+        const float l2 = dx * dx + dy * dy;
         if (l2 == 0.f) continue;                          // zero-length slice (G5)
-        float inv_len = rsqrtf(l2);
-        float cs = dx * inv_len, sn = dy * inv_len;
-        float x0 = cs * e0x + sn * e0y;
-        float y = -sn * e0x + cs * e0y;
-        float x1 = x0 + l2 * inv_len;                     // x0 + |E1-E0|: consistent with the sign test
+        const float de0 = fmaf(dx, e0x, dy * e0y);        // |D| * x0
         // Steps 3-4: distances of E0, E1 from the axis; single range [min, max).
         float r0 = fast_sqrt(e0x * e0x + e0y * e0y), r1 = fast_sqrt(e1x * e1x + e1y * e1y);
         int c_min = first_at_or_above(fminf(r0, r1), g.inv_delta, -0.5f, N);
         int c_max = first_at_or_above(fmaxf(r0, r1), g.inv_delta, -0.5f, N);
         int *row = acc + r * N;
-        // Steps 5-6: double range [|C|, min) iff the x signs differ (x = 0 non-negative).
-        if (x0 < 0.f && x1 >= 0.f) {
+        // Steps 5-6: double range [|C|, min) iff the x signs differ (x = 0 non-negative);
+        // |C| = |rotated y| = |D x E0| / |D|.
+        if (de0 < 0.f && de0 + l2 >= 0.f) {
+            const float y = fmaf(dx, e0y, -dy * e0x) * rsqrtf(l2);
             int c_c = min(first_at_or_above(fabsf(y), g.inv_delta, -0.5f, N), c_min);
             if (c_c == c_max) continue;
             if (c_c < N) atomicAdd(row + c_c, 2);
@@ -134,11 +134,12 @@ __device__ __forceinline__ void project_z(const Frame &f, const float *v, float 
     }
 }
 
+template <int K>
 __global__ void __launch_bounds__(kThreads)
 generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere, int64_t n_chunks,
                 const float4 *__restrict__ super_sphere, int64_t n_super,
                 const float *__restrict__ origins, const int *__restrict__ img_perm, int64_t n,
-                float R, int N, int K, uint16_t *__restrict__ out) {
+                float R, int N, uint16_t *__restrict__ out) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ Frame frames[kMaxK];
     __shared__ int img_idx[kMaxK];
@@ -316,17 +317,26 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
                     for (int c = 0; c < 9; ++c) v[c] = __ldg(src + c * kChunk);
                     // (image, triangle) pairs -- beta-extent test: does a layer centre
                     // lie in [z_min, z_max)?  Survivors go to the warp's queue.
-                    while (kmask) {
-                        const int k = __ffs(kmask) - 1;
-                        kmask &= kmask - 1;
-                        const Frame f = frames[k];
-                        float p[9], z[3];
-                        project_z(f, v, p, z);
-                        float zlo = fminf(z[0], fminf(z[1], z[2])), zhi = fmaxf(z[0], fmaxf(z[1], z[2]));
-                        const bool keep = first_at_or_above(zlo, g.inv_delta, g.row_off, N) <
-                                          first_at_or_above(zhi, g.inv_delta, g.row_off, N);
-                        unsigned m = __ballot_sync(0xffffffffu, keep);
-                        if (keep) queue[warp][qn + __popc(m & lt_mask)] = pack_item(chunk, lane, k);
+                    // the K images' tests are independent chains: computed together (ILP), then
+                    // pushed in image order
+                    bool keep[K];
+#pragma unroll
+                    for (int k = 0; k < K; ++k) {
+                        keep[k] = false;
+                        if ((kmask >> k) & 1u) {
+                            const Frame f = frames[k];
+                            float p[9], z[3];
+                            project_z(f, v, p, z);
+                            float zlo = fminf(z[0], fminf(z[1], z[2])), zhi = fmaxf(z[0], fmaxf(z[1], z[2]));
+                            keep[k] = first_at_or_above(zlo, g.inv_delta, g.row_off, N) <
+                                      first_at_or_above(zhi, g.inv_delta, g.row_off, N);
+                        }
+                    }
+#pragma unroll
+                    for (int k = 0; k < K; ++k) {
+                        if (!((kmask >> k) & 1u)) continue;
+                        unsigned m = __ballot_sync(0xffffffffu, keep[k]);
+                        if (keep[k]) queue[warp][qn + __popc(m & lt_mask)] = pack_item(chunk, lane, k);
                         qn += __popc(m);
                         if (qn >= 32) drain(32);
                     }
@@ -405,8 +415,12 @@ cudaError_t launch_generate(const DeviceMesh &m, const float *d_origins, int64_t
     if (n == 0) return cudaSuccess;
     const int K = generate_images_per_cta(N);
     size_t smem = (size_t)K * N * N * sizeof(int);
+    const void *kern = K >= 8 ? (const void *)generate_kernel<8> : K >= 4 ? (const void *)generate_kernel<4>
+                     : K >= 2 ? (const void *)generate_kernel<2> : (const void *)generate_kernel<1>;
+    const int Kt = K >= 8 ? 8 : K >= 4 ? 4 : K >= 2 ? 2 : 1;
+    smem = (size_t)Kt * N * N * sizeof(int);
     {
-        cudaError_t e = ensure_smem((const void *)generate_kernel, smem);
+        cudaError_t e = ensure_smem(kern, smem);
         if (e != cudaSuccess) return e;
     }
     // build the images in spatial order so a CTA's K support volumes are compact
@@ -414,9 +428,15 @@ cudaError_t launch_generate(const DeviceMesh &m, const float *d_origins, int64_t
     cudaError_t e = cudaMallocAsync((void **)&perm, sizeof(int) * n, s);
     if (e != cudaSuccess) return e;
     if ((e = spatial_order(d_origins, 6, n, perm, s)) != cudaSuccess) return e;
-    int64_t blocks = (n + K - 1) / K;
-    generate_kernel<<<(unsigned)blocks, kThreads, smem, s>>>(m.tri, m.sphere, m.n_chunks, m.super_sphere,
-                                                             m.n_super, d_origins, perm, n, R, N, K, d_out);
+    int64_t blocks = (n + Kt - 1) / Kt;
+#define RICI_GEN_LAUNCH(KK)                                                                             \
+    generate_kernel<KK><<<(unsigned)blocks, kThreads, smem, s>>>(m.tri, m.sphere, m.n_chunks, m.super_sphere, \
+                                                                 m.n_super, d_origins, perm, n, R, N, d_out)
+    if (Kt == 8) RICI_GEN_LAUNCH(8);
+    else if (Kt == 4) RICI_GEN_LAUNCH(4);
+    else if (Kt == 2) RICI_GEN_LAUNCH(2);
+    else RICI_GEN_LAUNCH(1);
+#undef RICI_GEN_LAUNCH
     note_launches(1);
     e = cudaGetLastError();
     cudaFreeAsync(perm, s);
