@@ -150,7 +150,9 @@ bool valid_bins(int32_t n_bins) { return n_bins >= 2 && n_bins <= 128; }
 // a9-a12 counts: tensor-core path for N = 64 (exact, with SIMT fallback inside), else SIMT.
 cudaError_t count_below(const void *dn, int64_t nn, const void *dh, int64_t nh, int N, const uint64_t *thr,
                         uint32_t *counts, cudaStream_t s) {
-    if (rici::use_mma_path(N)) {
+    // the tensor path streams 16-byte vectors of both image arrays
+    const bool aligned = ((reinterpret_cast<uintptr_t>(dn) | reinterpret_cast<uintptr_t>(dh)) & 15) == 0;
+    if (aligned && rici::use_mma_path(N)) {
         cudaError_t e = rici::launch_crss_count_mma((const uint16_t *)dn, nn, (const uint16_t *)dh, nh, thr, counts, s);
         if (e != cudaErrorNotSupported) return e;
         cudaGetLastError();

@@ -59,7 +59,7 @@ crss_pairs_kernel(const uint16_t *__restrict__ needles, int64_t nn, const uint16
     const int64_t P = (int64_t)N * N;
     const uint16_t *a = needles + i * P, *b = hay + j * P;
     uint64_t acc = 0;
-    if ((N % 8) == 0) {
+    if ((N % 8) == 0 && ((reinterpret_cast<uintptr_t>(needles) | reinterpret_cast<uintptr_t>(hay)) & 15) == 0) {
         // 8 pixels per lane per step (16-byte loads); the left neighbour of a run is the
         // previous lane's last pixel (P:497 shuffle), or the row's own first pixel at column 0
         for (int64_t base = 0; base < P; base += 256) {       // warp-uniform trip count
@@ -280,7 +280,8 @@ crss_tile_kernel(TileArgs A) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int N = A.N, P = N * N;
     int *seg0 = segbuf_all + warp * 2 * kSeg;
-    const bool vec_stage = (N % 8) == 0;
+    // 16-byte staging loads need N % 8 == 0 and a 16-byte aligned haystack base
+    const bool vec_stage = (N % 8) == 0 && (reinterpret_cast<uintptr_t>(A.hay) & 15) == 0;
 
     for (;;) {
         __syncthreads();

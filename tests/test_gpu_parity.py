@@ -426,3 +426,20 @@ def test_saturation_at_65535(rici, oracle_mod):
     assert np.array_equal(d, oracle_mod.crss_matrix(g, g))
     r = rici.rici_crss_search(_dev(g), _dev(g)).cpu().numpy()
     assert np.array_equal(r.astype(np.uint32), oracle_mod.ranks(g, g))
+
+
+def test_unaligned_image_buffers(rici, oracle_mod):
+    """Image arrays that start 2 bytes past a 16-byte boundary (legal uint16 pointers) take the
+    scalar paths and stay exact."""
+    rng = np.random.default_rng(11)
+    A = _rand_imgs(rng, 40, density=0.2)
+    H = np.concatenate([A, _rand_imgs(rng, 50, density=0.3)])
+    nbuf = torch.zeros(A.size + 1, dtype=torch.int16, device=DEV)
+    hbuf = torch.zeros(H.size + 1, dtype=torch.int16, device=DEV)
+    nbuf[1:] = _dev(A).reshape(-1)
+    hbuf[1:] = _dev(H).reshape(-1)
+    nv, hv = nbuf[1:].view(40, 64, 64), hbuf[1:].view(90, 64, 64)
+    assert nv.data_ptr() % 16 == 2
+    assert np.array_equal(rici.rici_crss_search(nv, hv).cpu().numpy().astype(np.uint32), oracle_mod.ranks(A, H))
+    d = rici.rici_crss_distances(nv, hv).cpu().numpy().view(np.uint64)
+    assert np.array_equal(d, oracle_mod.crss_matrix(A, H))
