@@ -7,22 +7,21 @@
 //     D_x(r,c) = x[r][c] - x[r][c-1].
 // The rank of needle i is #{ j : CRSS(n_i,h_j) < CRSS(n_i,h_i) } (best tie P:459).
 //
-// B200 design (DESIGN.md "CRSS kernels"):
-//  a9  needle preprocessing: one warp per needle compacts the needle's change mask
-//      (D_n != 0) into a list of packed (D_n, pixel) entries with a warp ballot --
-//      the mask held as the list of its set positions.  Typical needles change in
-//      2-7% of their 4032 deltas.
-//  a11 streaming compare: a CTA stages a tile of 32 haystack images as int8 D_h
-//      planes in shared memory (one plane per lane, padded so the 32 lanes hit 32
-//      distinct banks) and every warp walks needle lists against it: lane j
-//      accumulates needle i vs haystack image j, integer-only.  The left
-//      neighbour for D_h is formed once per staged pixel, never re-read per pair.
-//  a12 rank: pred = CRSS < t_i, __ballot_sync + __popc per 32 images, counts kept
-//      in shared memory per needle and flushed once per work item.
-// Exactness: the int8 / uint32 fast path is taken only when every pixel of the
-// needle and of the haystack tile is <= 127, which bounds each term by 254^2 and a
-// full sum by 4032 * 254^2 < 2^32; otherwise the pair runs the 64-bit path from
-// global memory.  Both give the exact uint64 CRSS for every input.
+// This is the general SIMT path (every N; the exact fallback of the tensor-core path in
+// crss_mma.cu for images outside its int8 guard; RICI_CRSS_SIMT / RICI_CRSS_EARLY_EXIT).
+// B200 design (DESIGN.md 6.3):
+//  a9  needle preprocessing: one warp per needle compacts the needle's change mask (D_n != 0)
+//      into a CSR list of packed (D_n, pixel) entries with a warp ballot -- the mask held as
+//      the list of its set positions (typically 2-7% of the 4032 deltas), in decreasing-|D_n|
+//      buckets, padded to a multiple of 8 with zero terms and closed by a marker entry.
+//  a11 streaming compare: a CTA stages a tile of 32 haystack images as int8 D_h planes in
+//      shared memory (one power-of-two plane per lane, XOR-swizzled so the 32 lanes hit 32
+//      distinct banks; the left neighbour comes from the previous lane).  Each warp
+//      streams one contiguous run of needle lists (cp.async, double-buffered) and lane j
+//      accumulates needle i vs haystack image j, integer-only: 4 instructions per entry.
+//  a12 rank: pred = CRSS < t_i, __ballot_sync + __popc per 32 images, counts kept in shared
+//      memory per needle and flushed once per work item.  Rank mode stops a needle
+//      once every lane's partial sum is >= t_i.
 #include "rici_internal.cuh"
 
 namespace rici {
@@ -195,7 +194,7 @@ needle_fill_kernel(const uint16_t *__restrict__ needles, int64_t nn, int N,
 // ---------------------------------------------------------------- a11 + a12: tiles
 struct TileArgs {
     const uint16_t *hay; int64_t nh;
-    const uint16_t *needles; int64_t nn;
+    int64_t nn;
     const int *entries; const int64_t *off; const int *n_entries; const unsigned char *small;
     const uint64_t *thr; uint32_t *counts; uint64_t *dist;
     int N, plane_bytes, use_smem, early_exit;
@@ -508,7 +507,7 @@ cudaError_t launch_crss_search_tiles(const uint16_t *d_needles, int64_t nn,
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
 
     TileArgs A;
-    A.hay = d_haystack; A.nh = nh; A.needles = d_needles; A.nn = nn;
+    A.hay = d_haystack; A.nh = nh; A.nn = nn;
     A.entries = entries; A.off = off; A.n_entries = n_entries; A.small = small;
     A.thr = d_thresholds; A.counts = d_counts; A.dist = d_dist;
     A.N = N;

@@ -10,17 +10,23 @@
 //      double range [|C|, min|E|) (six steps),
 //   3. increment the bins whose circle radius falls in those ranges.
 //
-// B200 design (DESIGN.md "Construction kernel"):
-//  * one CTA owns K images; their 32-bit counters live in shared memory as
-//    per-row DIFFERENCE arrays, so a segment costs <= 3 shared atomics (+2 at
-//    col(|C|), -1 at col(min), -1 at col(max)) instead of one per covered bin;
-//    a warp-shuffle prefix scan per row turns them into counts in the epilogue;
-//  * triangles stream from the chunked mesh buffer (mesh.cu); each chunk's
-//    bounding sphere is tested against the CTA's union of support spheres and
-//    chunks that cannot touch any image are skipped (exact: they add 0);
-//  * the per-image rotation coefficients are computed once per image in the
-//    CTA prologue ("out of the inner loop");
-//  * saturation to uint16 (G9) and coalesced 128-bit stores in the epilogue.
+// B200 design (DESIGN.md 6.1):
+//  * one CTA owns K images (K = 2 at N = 64); their 32-bit counters live in shared memory
+//    as per-row DIFFERENCE arrays, so a segment costs <= 3 shared atomics (+2 at col(|C|),
+//    -1 at col(min), -1 at col(max)) instead of one per covered bin; a warp-shuffle prefix
+//    scan per row turns them into counts in the epilogue;
+//  * images are built in spatial (Morton-cell) order and the mesh is stored in spatially
+//    compact chunks of 32 triangles (mesh.cu, sort.cu); an exact three-level cull skips
+//    triangles that cannot reach any of the CTA's support volumes: superchunk spheres and
+//    chunk spheres vs the CTA sphere, then chunk sphere vs each image's support CYLINDER;
+//  * (image, triangle) pairs that pass the beta-extent test are compacted into a
+//    per-warp queue (ballot + popc) and drained 32 at a time, one pair per lane, so the
+//    divergent per-layer work runs with full warps; an alpha-box test skips triangles whose
+//    (T_x, T_y) box misses the support disk;
+//  * the per-image rotation coefficients are computed once per image in the CTA prologue
+//    ("out of the inner loop");
+//  * saturation to uint16 (G9) and coalesced 128-bit stores in the epilogue, each image to
+//    its caller index.
 #include <cstdlib>
 
 #include "frame.cuh"

@@ -1,12 +1,16 @@
 // mesh.cu -- (a1) mesh staging for the construction kernel.
 //
-// "iterate over each triangle in the scene": the construction kernel
-// streams every triangle once per group of images, so the indexed mesh
-// (vertices + index triples, D1) is de-indexed once into a device buffer laid
-// out for that stream: chunks of 32 triangles, structure-of-arrays inside a
-// chunk so one warp reads a chunk with nine coalesced 128-byte loads, plus a
-// bounding sphere per chunk that lets a CTA skip chunks that cannot reach any
-// of its images' support cylinders (an exact cull: such triangles add 0).
+// "iterate over each triangle in the scene": the construction kernel streams every
+// triangle once per group of images, so the indexed mesh (vertices + index triples, D1) is
+// de-indexed once into a device buffer laid out for that stream:
+//  * triangles in spatial order (an 18-bit Morton cell of the centroid, counting sort in
+//    sort.cu) -- an internal reordering that cannot change any image, counts being sums
+//    over triangles; the permutation is kept for per-triangle tags (rici_clutter_fraction);
+//  * chunks of 32 triangles, structure-of-arrays inside a chunk, so one warp reads a chunk
+//    with nine coalesced 128-byte loads;
+//  * a bounding sphere per chunk and per superchunk (32 chunks) that let the construction
+//    and clutter kernels skip triangles that cannot reach a support volume (an exact cull:
+//    such triangles add 0).
 #include <algorithm>
 
 #include "rici_internal.cuh"
