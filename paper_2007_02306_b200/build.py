@@ -13,6 +13,8 @@ SOURCES = ["abi.cu", "mesh.cu", "sort.cu", "generate.cu", "crss.cu", "crss_mma.c
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC,-fvisibility=hidden", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
+# tuning sweeps only (scripts/gen_variant_sweep.py): extra -D defines for a throwaway build
+FLAGS += os.environ.get("RICI_NVCC_DEFINES", "").split()
 
 
 def _stale() -> bool:

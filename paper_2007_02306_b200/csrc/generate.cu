@@ -11,10 +11,11 @@
 //   3. increment the bins whose circle radius falls in those ranges.
 //
 // B200 design:
-//  * one CTA owns K images (K = 2 at N = 64); their 32-bit counters live in shared memory
-//    as per-row DIFFERENCE arrays, so a segment costs <= 3 shared atomics (+2 at col(|C|),
-//    -1 at col(min), -1 at col(max)) instead of one per covered bin; a warp-shuffle prefix
-//    scan per row turns them into counts in the epilogue;
+//  * one CTA owns K images (K = 2 at N = 64, 5 CTAs / SM); their 32-bit counters live in
+//    shared memory as per-row DIFFERENCE arrays of N+1 columns (column N a sink), so a
+//    segment costs <= 3 branch-free shared reductions (+2 at col(|C|), -1 at col(min), -1 at
+//    col(max)) instead of one per covered bin; a warp-shuffle prefix scan per row turns them
+//    into counts in the epilogue;
 //  * images are built in spatial (Morton-cell) order and the mesh is stored in spatially
 //    compact chunks of 32 triangles (mesh.cu, sort.cu); an exact three-level cull skips
 //    triangles that cannot reach any of the CTA's support volumes: superchunk spheres and
@@ -23,10 +24,12 @@
 //    per-warp queue (ballot + popc) and drained 32 at a time, one pair per lane, so the
 //    divergent per-layer work runs with full warps; an alpha-box test skips triangles whose
 //    (T_x, T_y) box misses the support disk;
+//  * chunk survivors carry their per-image cylinder hits (one 32-bit entry), and each warp
+//    prefetches its next chunk's triangles while it processes the current one;
 //  * the per-image rotation coefficients are computed once per image in the CTA prologue
 //    ("out of the inner loop");
-//  * saturation to uint16 (G9) and coalesced 128-bit stores in the epilogue, each image to
-//    its caller index.
+//  * saturation to uint16 (G9) fused into the prefix-scan epilogue: each row is stored
+//    straight to its image's caller index as packed 32-bit pairs.
 #include <cstdlib>
 
 #include "frame.cuh"
@@ -34,6 +37,13 @@
 
 namespace rici {
 namespace {
+
+#if RICI_GEN_STATS   // tuning builds only: event counters read by rici_debug_gen_stats
+__device__ unsigned long long g_stats[8];
+#define RICI_STAT(i, v) atomicAdd(&g_stats[i], (unsigned long long)(v))
+#else
+#define RICI_STAT(i, v)
+#endif
 
 constexpr int kThreads = 256;
 constexpr int kMaxK = 8;
@@ -43,11 +53,14 @@ constexpr int kChunkCap = 1024;          // chunk survivors per batch (multiple 
 // First index i in [0, n] with (i + 1/2) * delta + off >= v, i.e. ceil(v/delta - off/delta - 1/2).
 // Used for rows (off = -R/2: beta_r >= v) and columns (off = 0: rho_c >= v).  Exact ties are
 // fragile pixels; the row loop re-checks membership with explicit comparisons.
+// cvt.rpi.s32.f32 is ceil with saturation (NaN -> 0), so one conversion replaces clamp + ceil.
 __device__ __forceinline__ int first_at_or_above(float v, float inv_delta, float off_scaled, int n) {
-    float x = fmaf(v, inv_delta, off_scaled);        // v/delta - off/delta - 1/2
-    x = fminf(fmaxf(x, -1.0f), (float)n + 1.0f);
-    int i = (int)ceilf(x);
+    const int i = __float2int_ru(fmaf(v, inv_delta, off_scaled));   // v/delta - off/delta - 1/2
     return min(max(i, 0), n);
+}
+// The same for v >= 0 and off = 0 (columns): the argument is >= -1/2, so the ceiling is >= 0.
+__device__ __forceinline__ int first_col_at_or_above(float v, float inv_delta, int n) {
+    return min(__float2int_ru(fmaf(v, inv_delta, -0.5f)), n);
 }
 
 __device__ __forceinline__ void sort3(float &ax, float &ay, float &az, float &bx, float &by,
@@ -66,11 +79,22 @@ struct Geometry {
 };
 
 __device__ __forceinline__ float fast_sqrt(float x) { return x > 0.f ? x * rsqrtf(x) : 0.f; }
+__device__ __forceinline__ float fast_rcp(float x) {      // MUFU.RCP, ~1 ulp
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+// Shared-memory reduction on a 32-bit shared-window address (no generic->shared conversion).
+__device__ __forceinline__ void red_shared(unsigned addr, int v) {
+    asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
 
 // Steps 1-6 for every layer of one projected, z-sorted triangle, accumulated
 // into the image's per-row difference arrays.  Approximate reciprocals / square roots
 // (relative error ~1e-7) move decisions by far less than the 1e-5*R attribution bound.
-__device__ __forceinline__ void rasterise_triangle(int *__restrict__ acc, const Geometry &g,
+// `acc` is the image's [N][N+1] difference array as a shared-window address: column N is a
+// sink, so a range end at N needs no test, and coinciding ends cancel in place.
+__device__ __forceinline__ void rasterise_triangle(unsigned acc, const Geometry &g,
                                                    float ax, float ay, float az, float bx,
                                                    float by, float bz, float cx, float cy,
                                                    float cz) {
@@ -78,10 +102,12 @@ __device__ __forceinline__ void rasterise_triangle(int *__restrict__ acc, const 
     int r_lo = first_at_or_above(az, g.inv_delta, g.row_off, N);
     int r_hi = first_at_or_above(cz, g.inv_delta, g.row_off, N);
     if (r_lo >= r_hi) return;
-    const float inv_ac = __frcp_rn(cz - az);             // > 0 whenever a layer is inside
-    const float inv_ab = bz > az ? __frcp_rn(bz - az) : 0.f;
-    const float inv_bc = cz > bz ? __frcp_rn(cz - bz) : 0.f;
-    for (int r = r_lo; r < r_hi; ++r) {
+    RICI_STAT(4, r_hi - r_lo);
+    const float inv_ac = fast_rcp(cz - az);              // > 0 whenever a layer is inside
+    const float inv_ab = bz > az ? fast_rcp(bz - az) : 0.f;
+    const float inv_bc = cz > bz ? fast_rcp(cz - bz) : 0.f;
+    unsigned row = acc + 4u * (unsigned)(r_lo * (N + 1));
+    for (int r = r_lo; r < r_hi; ++r, row += 4u * (unsigned)(N + 1)) {
         float beta = fmaf((float)r + 0.5f, g.delta, -g.half_r);
         if (!(az <= beta && beta < cz)) continue;        // layer membership, half-open (G5)
         // Step 1: E0 on the long edge (a,c), E1 on (a,b) below / (b,c) above the middle vertex.
@@ -104,23 +130,22 @@ __device__ __forceinline__ void rasterise_triangle(int *__restrict__ acc, const 
         const float de0 = fmaf(dx, e0x, dy * e0y);        // |D| * x0
         // Steps 3-4: distances of E0, E1 from the axis; single range [min, max).
         float r0 = fast_sqrt(e0x * e0x + e0y * e0y), r1 = fast_sqrt(e1x * e1x + e1y * e1y);
-        int c_min = first_at_or_above(fminf(r0, r1), g.inv_delta, -0.5f, N);
-        int c_max = first_at_or_above(fmaxf(r0, r1), g.inv_delta, -0.5f, N);
-        int *row = acc + r * N;
+        const int c_min = first_col_at_or_above(fminf(r0, r1), g.inv_delta, N);
+        const int c_max = first_col_at_or_above(fmaxf(r0, r1), g.inv_delta, N);
         // Steps 5-6: double range [|C|, min) iff the x signs differ (x = 0 non-negative);
-        // |C| = |rotated y| = |D x E0| / |D|.
-        if (de0 < 0.f && de0 + l2 >= 0.f) {
+        // |C| = |rotated y| = |D x E0| / |D|.  Single: +1 at c_min, -1 at c_max.  Double:
+        // +2 at c_c, -1 at c_min, -1 at c_max.  Empty ranges cancel at one address.
+        const bool dbl = de0 < 0.f && de0 + l2 >= 0.f;
+        int c_lo = c_min;
+        if (dbl) {
             const float y = fmaf(dx, e0y, -dy * e0x) * rsqrtf(l2);
-            int c_c = min(first_at_or_above(fabsf(y), g.inv_delta, -0.5f, N), c_min);
-            if (c_c == c_max) continue;
-            if (c_c < N) atomicAdd(row + c_c, 2);
-            if (c_min < N) atomicAdd(row + c_min, -1);
-            if (c_max < N) atomicAdd(row + c_max, -1);
-        } else {
-            if (c_min == c_max) continue;
-            atomicAdd(row + c_min, 1);                    // c_min < c_max <= N
-            if (c_max < N) atomicAdd(row + c_max, -1);
+            c_lo = min(first_col_at_or_above(fabsf(y), g.inv_delta, N), c_min);
         }
+        if (c_lo == c_max) continue;                      // nothing in [c_lo, c_max)
+        RICI_STAT(5, 1);
+        red_shared(row + 4u * (unsigned)c_lo, dbl ? 2 : 1);
+        if (dbl) red_shared(row + 4u * (unsigned)c_min, -1);
+        red_shared(row + 4u * (unsigned)c_max, -1);
     }
 }
 
@@ -140,28 +165,32 @@ __device__ __forceinline__ void project_z(const Frame &f, const float *v, float 
     }
 }
 
+// K <= 2 (N = 64 default): 32 KB of counters, so smem admits 5 CTAs / SM; cap the registers
+// (48, a few bytes of spill) so the register file admits them too -- measured 3.34 -> 3.09 ms on C2
 template <int K>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, K <= 2 ? 5 : 1)
 generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere, int64_t n_chunks,
                 const float4 *__restrict__ super_sphere, int64_t n_super,
                 const float *__restrict__ origins, const int *__restrict__ img_perm, int64_t n,
-                float R, int N, uint16_t *__restrict__ out) {
+                float R, int N, const Geometry g, uint16_t *__restrict__ out) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ Frame frames[kMaxK];
     __shared__ int img_idx[kMaxK];
     __shared__ int list[kListCap];
-    __shared__ int list_n, list_next, chunk_n;
-    __shared__ int chunk_list[kChunkCap];
+    __shared__ int list_n, chunk_n;
+    __shared__ unsigned chunk_list[kChunkCap];   // (chunk << 8) | image mask
     __shared__ float cta_sphere[4];
     __shared__ int queue[kThreads / 32][2 * 32];
 
-    int *acc = reinterpret_cast<int *>(smem_raw);        // [K][N][N] difference arrays
+    int *acc = reinterpret_cast<int *>(smem_raw);        // [K][N][N+1] difference arrays
+    const unsigned acc_s = (unsigned)__cvta_generic_to_shared(acc);
+    const int img_words = N * (N + 1);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned lt_mask = (1u << lane) - 1u;
     const int64_t img0 = (int64_t)blockIdx.x * K;
     const int k_valid = (int)min((int64_t)K, n - img0);
 
-    for (int i = tid; i < K * N * N; i += kThreads) acc[i] = 0;
+    for (int i = tid; i < K * img_words; i += kThreads) acc[i] = 0;
     if (tid < K) {
         if (tid < k_valid) {
             const int idx = img_perm ? img_perm[img0 + tid] : (int)(img0 + tid);
@@ -199,13 +228,6 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
     }
     __syncthreads();
 
-    Geometry g;
-    g.n = N;
-    g.delta = R / (float)N;
-    g.inv_delta = (float)N / R;
-    g.half_r = 0.5f * R;
-    g.r2 = R * R;
-    g.row_off = 0.5f * (float)N - 0.5f;
     const float cs_r = cta_sphere[3];
     int qn = 0;                                          // warp-uniform queue length
 
@@ -219,6 +241,7 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
         if (lane < rest) queue[warp][lane] = moved;
         qn = rest;
         if (item >= 0) {
+            RICI_STAT(2, 1);
             const int64_t chunk = (int64_t)((unsigned)item >> 8);
             const int t = (item >> 3) & 31, k = item & 7;
             const float *src = tri + chunk * 9 * kChunk + t;
@@ -240,10 +263,11 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
             const float bx0 = fmaxf(fmaxf(fminf(x[0], fminf(x[1], x[2])), -fmaxf(x[0], fmaxf(x[1], x[2]))), 0.f);
             const float by0 = fmaxf(fmaxf(fminf(y[0], fminf(y[1], y[2])), -fmaxf(y[0], fmaxf(y[1], y[2]))), 0.f);
             if (bx0 * bx0 + by0 * by0 <= g.r2) {
+                RICI_STAT(3, 1);
                 float ax = x[0], ay = y[0], az = z[0], bx = x[1], by = y[1], bz = z[1],
                       cx = x[2], cy = y[2], cz = z[2];
                 sort3(ax, ay, az, bx, by, bz, cx, cy, cz);
-                rasterise_triangle(acc + k * N * N, g, ax, ay, az, bx, by, bz, cx, cy, cz);
+                rasterise_triangle(acc_s + 4u * (unsigned)(k * img_words), g, ax, ay, az, bx, by, bz, cx, cy, cz);
             }
         }
         __syncwarp();
@@ -254,7 +278,7 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
         const float pad_r = 1e-4f * R;
         // Level 1: superchunks (kSuper*kChunk triangles) whose sphere meets the CTA sphere.
         for (int64_t base = 0; base < n_super; base += kListCap) {
-            if (tid == 0) { list_n = 0; list_next = 0; chunk_n = 0; }
+            if (tid == 0) { list_n = 0; chunk_n = 0; }
             __syncthreads();
             for (int q = 0; q < kListCap / kThreads; ++q) {
                 int64_t c = base + q * kThreads + tid;
@@ -278,49 +302,63 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
                 const int sc1 = min(n_sc, sc0 + kChunkCap / kSuper);
                 for (int e = sc0 + warp; e < sc1; e += kThreads / 32) {
                     const int64_t c_lane = (base + list[e]) * kSuper + lane;
-                    bool ck = false;
+                    // chunk sphere vs the CTA sphere, then vs each image's support CYLINDER
+                    // (r <= R, |beta| <= R/2); the per-image hits travel with the chunk id
+                    unsigned kbits = 0;
                     if (c_lane < n_chunks) {
-                        float4 s4 = sphere[c_lane];
+                        const float4 s4 = sphere[c_lane];
                         float dx = s4.x - ccx, dy = s4.y - ccy, dz = s4.z - ccz;
                         float rr = s4.w + cs_r;
-                        ck = dx * dx + dy * dy + dz * dz <= rr * rr;
+                        if (dx * dx + dy * dy + dz * dz <= rr * rr) {
+                            const float pad = pad_r + 1e-6f * (fabsf(s4.x) + fabsf(s4.y) + fabsf(s4.z) + s4.w);
+                            const float ra = R + s4.w + pad, hb = 0.5f * R + s4.w + pad;
+#pragma unroll
+                            for (int k = 0; k < K; ++k) {
+                                const Frame &f = frames[k];
+                                if (k >= k_valid || f.valid == 0.f) continue;
+                                float ex = s4.x - f.sx, ey = s4.y - f.sy, ez = s4.z - f.sz;
+                                float b = fmaf(f.czx, ex, fmaf(f.czy, ey, f.czz * ez));
+                                float a2 = fmaxf(ex * ex + ey * ey + ez * ez - b * b, 0.f);
+                                if (fabsf(b) <= hb && a2 <= ra * ra) kbits |= 1u << k;
+                            }
+                        }
                     }
+                    const bool ck = kbits != 0;
                     unsigned m = __ballot_sync(0xffffffffu, ck);
                     int pos = 0;
                     if (lane == 0 && m) pos = atomicAdd(&chunk_n, __popc(m));
                     pos = __shfl_sync(0xffffffffu, pos, 0);
-                    if (ck) chunk_list[pos + __popc(m & lt_mask)] = c_lane;
+                    if (ck) chunk_list[pos + __popc(m & lt_mask)] = ((unsigned)c_lane << 8) | kbits;
                 }
                 __syncthreads();
                 const int n_ck = chunk_n;
-                // Level 3 (dynamically scheduled, one chunk per warp at a time).
-                for (;;) {
-                    int e = 0;
-                    if (lane == 0) e = atomicAdd(&list_next, 1);
-                    e = __shfl_sync(0xffffffffu, e, 0);
-                    if (e >= n_ck) break;
-                    const int64_t chunk = chunk_list[e];
-                    // images whose support CYLINDER (r <= R, |beta| <= R/2) the chunk sphere meets
-                    unsigned kmask;
-                    {
-                        bool hit = false;
-                        if (lane < k_valid && frames[lane].valid != 0.f) {
-                            const Frame f = frames[lane];
-                            float4 s4 = sphere[chunk];
-                            float dx = s4.x - f.sx, dy = s4.y - f.sy, dz = s4.z - f.sz;
-                            float b = fmaf(f.czx, dx, fmaf(f.czy, dy, f.czz * dz));
-                            float a2 = fmaxf(dx * dx + dy * dy + dz * dz - b * b, 0.f);
-                            float pad = pad_r + 1e-6f * (fabsf(s4.x) + fabsf(s4.y) + fabsf(s4.z) + s4.w);
-                            float ra = R + s4.w + pad;
-                            hit = fabsf(b) <= 0.5f * R + s4.w + pad && a2 <= ra * ra;
-                        }
-                        kmask = __ballot_sync(0xffffffffu, hit);
-                    }
-                    if (kmask == 0) continue;
-                    const float *src = tri + chunk * 9 * kChunk + lane;
+                // Level 3: static round-robin over the warps, so each warp knows its next chunk
+                // and prefetches its nine triangle planes while the current one is processed
+                // (measured faster than a shared-counter schedule with the same prefetch).
+                int e = warp;
+                unsigned nxt_ent = 0;
+                float nv9[9];
+                if (e < n_ck) {
+                    nxt_ent = chunk_list[e];
+                    const float *src = tri + (int64_t)(nxt_ent >> 8) * 9 * kChunk + lane;
+#pragma unroll
+                    for (int c = 0; c < 9; ++c) nv9[c] = __ldg(src + c * kChunk);
+                }
+                while (e < n_ck) {
+                    const unsigned ent = nxt_ent;
+                    const int64_t chunk = (int64_t)(ent >> 8);
+                    const unsigned kmask = ent & 0xffu;
+                    if (lane == 0) { RICI_STAT(0, 1); RICI_STAT(1, __popc(kmask)); }
                     float v[9];
 #pragma unroll
-                    for (int c = 0; c < 9; ++c) v[c] = __ldg(src + c * kChunk);
+                    for (int c = 0; c < 9; ++c) v[c] = nv9[c];
+                    e += kThreads / 32;
+                    if (e < n_ck) {
+                        nxt_ent = chunk_list[e];
+                        const float *src = tri + (int64_t)(nxt_ent >> 8) * 9 * kChunk + lane;
+#pragma unroll
+                        for (int c = 0; c < 9; ++c) nv9[c] = __ldg(src + c * kChunk);
+                    }
                     // (image, triangle) pairs -- beta-extent test: does a layer centre
                     // lie in [z_min, z_max)?  Survivors go to the warp's queue.
                     // the K images' tests are independent chains: computed together (ILP), then
@@ -348,7 +386,7 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
                     }
                 }
                 __syncthreads();
-                if (tid == 0) { chunk_n = 0; list_next = 0; }
+                if (tid == 0) chunk_n = 0;
                 __syncthreads();
             }
         }
@@ -356,10 +394,15 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
     }
     __syncthreads();
 
-    // Epilogue 1: per-row inclusive prefix sum of the difference arrays (warp per row).
+    // Epilogue: per-row inclusive prefix sum of the difference arrays (warp per row), then
+    // saturate to uint16 (G9) and store the row at its image's caller index -- lane l holds
+    // columns [l*cpl, l*cpl + cpl), written as packed pairs when aligned.
+    const int npix = N * N;
     const int cpl = (N + 31) / 32;                 // columns per lane
+    const bool pairs = (cpl % 2) == 0 && (N % 2) == 0 && (reinterpret_cast<uintptr_t>(out) & 3) == 0;
     for (int row = warp; row < k_valid * N; row += kThreads / 32) {
-        int *rp = acc + row * N;
+        const int k = row / N, r = row - k * N;
+        const int *rp = acc + k * img_words + r * (N + 1);
         unsigned vals[4];
         unsigned local = 0;
         for (int j = 0; j < cpl; ++j) {
@@ -373,35 +416,20 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
             unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += t;
         }
-        unsigned excl = incl - local;
-        for (int j = 0; j < cpl; ++j) {
-            int c = lane * cpl + j;
-            if (c < N) rp[c] = (int)(vals[j] + excl);
-        }
-    }
-    __syncthreads();
-
-    // Epilogue 2: saturate to uint16 (G9) and store each image at its caller index;
-    // 128-bit stores when aligned.
-    const int npix = N * N;
-    const unsigned *cnt = reinterpret_cast<const unsigned *>(acc);
-    const bool vec = (npix % 8) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
-    for (int k = 0; k < k_valid; ++k) {
-        uint16_t *dst = out + (int64_t)img_idx[k] * npix;
-        const unsigned *src = cnt + k * npix;
-        if (vec) {
-            for (int i = tid * 8; i < npix; i += kThreads * 8) {
-                uint4 a = *reinterpret_cast<const uint4 *>(src + i);
-                uint4 b = *reinterpret_cast<const uint4 *>(src + i + 4);
-                uint4 o;
-                o.x = min(a.x, 65535u) | (min(a.y, 65535u) << 16);
-                o.y = min(a.z, 65535u) | (min(a.w, 65535u) << 16);
-                o.z = min(b.x, 65535u) | (min(b.y, 65535u) << 16);
-                o.w = min(b.z, 65535u) | (min(b.w, 65535u) << 16);
-                *reinterpret_cast<uint4 *>(dst + i) = o;
+        const unsigned excl = incl - local;
+        uint16_t *dst = out + (int64_t)img_idx[k] * npix + (int64_t)r * N;
+        if (pairs) {
+            for (int j = 0; j < cpl; j += 2) {
+                int c = lane * cpl + j;
+                if (c < N)
+                    *reinterpret_cast<unsigned *>(dst + c) =
+                        min(vals[j] + excl, 65535u) | (min(vals[j + 1] + excl, 65535u) << 16);
             }
         } else {
-            for (int i = tid; i < npix; i += kThreads) dst[i] = (uint16_t)min(src[i], 65535u);
+            for (int j = 0; j < cpl; ++j) {
+                int c = lane * cpl + j;
+                if (c < N) dst[c] = (uint16_t)min(vals[j] + excl, 65535u);
+            }
         }
     }
 }
@@ -409,8 +437,8 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
 }  // namespace
 
 int generate_images_per_cta(int N) {
-    int per = N * N * 4;
-    int budget = 64 * 1024;                       // counters per CTA (3 CTAs / SM at N = 64)
+    int per = N * (N + 1) * 4;
+    int budget = 34 * 1024;                       // counters per CTA (K = 2, 5 CTAs / SM at N = 64)
     if (const char *v = getenv("RICI_GEN_SMEM_KB")) budget = atoi(v) * 1024;   // tuning knob
     int k = budget / per;
     return k < 1 ? 1 : (k > kMaxK ? kMaxK : k);
@@ -420,11 +448,11 @@ cudaError_t launch_generate(const DeviceMesh &m, const float *d_origins, int64_t
                             uint16_t *d_out, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     const int K = generate_images_per_cta(N);
-    size_t smem = (size_t)K * N * N * sizeof(int);
+    size_t smem = (size_t)K * N * (N + 1) * sizeof(int);
     const void *kern = K >= 8 ? (const void *)generate_kernel<8> : K >= 4 ? (const void *)generate_kernel<4>
                      : K >= 2 ? (const void *)generate_kernel<2> : (const void *)generate_kernel<1>;
     const int Kt = K >= 8 ? 8 : K >= 4 ? 4 : K >= 2 ? 2 : 1;
-    smem = (size_t)Kt * N * N * sizeof(int);
+    smem = (size_t)Kt * N * (N + 1) * sizeof(int);
     {
         cudaError_t e = ensure_smem(kern, smem);
         if (e != cudaSuccess) return e;
@@ -435,9 +463,17 @@ cudaError_t launch_generate(const DeviceMesh &m, const float *d_origins, int64_t
     if (e != cudaSuccess) return e;
     if ((e = spatial_order(d_origins, 6, n, perm, s)) != cudaSuccess) return e;
     int64_t blocks = (n + Kt - 1) / Kt;
+    // the geometry lives in the kernel's parameter bank (no per-thread recomputation)
+    Geometry g;
+    g.n = N;
+    g.delta = R / (float)N;
+    g.inv_delta = (float)N / R;
+    g.half_r = 0.5f * R;
+    g.r2 = R * R;
+    g.row_off = 0.5f * (float)N - 0.5f;
 #define RICI_GEN_LAUNCH(KK)                                                                             \
     generate_kernel<KK><<<(unsigned)blocks, kThreads, smem, s>>>(m.tri, m.sphere, m.n_chunks, m.super_sphere, \
-                                                                 m.n_super, d_origins, perm, n, R, N, d_out)
+                                                                 m.n_super, d_origins, perm, n, R, N, g, d_out)
     if (Kt == 8) RICI_GEN_LAUNCH(8);
     else if (Kt == 4) RICI_GEN_LAUNCH(4);
     else if (Kt == 2) RICI_GEN_LAUNCH(2);
@@ -450,3 +486,12 @@ cudaError_t launch_generate(const DeviceMesh &m, const float *d_origins, int64_t
 }
 
 }  // namespace rici
+
+#if RICI_GEN_STATS
+extern "C" __attribute__((visibility("default"))) int rici_debug_gen_stats(unsigned long long *out, int reset) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, rici::g_stats, sizeof(unsigned long long) * 8);
+    if (reset) { unsigned long long z[8] = {}; cudaMemcpyToSymbol(rici::g_stats, z, sizeof(z)); }
+    return 0;
+}
+#endif
