@@ -78,7 +78,11 @@ struct Geometry {
     int n;
 };
 
-__device__ __forceinline__ float fast_sqrt(float x) { return x > 0.f ? x * rsqrtf(x) : 0.f; }
+__device__ __forceinline__ float fast_sqrt(float x) {     // MUFU.SQRT, ~1 ulp; sqrt(0) = 0
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
 __device__ __forceinline__ float fast_rcp(float x) {      // MUFU.RCP, ~1 ulp
     float r;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
@@ -107,8 +111,10 @@ __device__ __forceinline__ void rasterise_triangle(unsigned acc, const Geometry 
     const float inv_ab = bz > az ? fast_rcp(bz - az) : 0.f;
     const float inv_bc = cz > bz ? fast_rcp(cz - bz) : 0.f;
     unsigned row = acc + 4u * (unsigned)(r_lo * (N + 1));
-    for (int r = r_lo; r < r_hi; ++r, row += 4u * (unsigned)(N + 1)) {
-        float beta = fmaf((float)r + 0.5f, g.delta, -g.half_r);
+    const unsigned row_step = 4u * (unsigned)(N + 1);
+    float rc = (float)r_lo + 0.5f;                        // r + 1/2, exact in float
+    for (int r = r_lo; r < r_hi; ++r, row += row_step, rc += 1.f) {
+        float beta = fmaf(rc, g.delta, -g.half_r);
         if (!(az <= beta && beta < cz)) continue;        // layer membership, half-open (G5)
         // Step 1: E0 on the long edge (a,c), E1 on (a,b) below / (b,c) above the middle vertex.
         float t = (beta - az) * inv_ac;
@@ -400,35 +406,36 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
     const int npix = N * N;
     const int cpl = (N + 31) / 32;                 // columns per lane
     const bool pairs = (cpl % 2) == 0 && (N % 2) == 0 && (reinterpret_cast<uintptr_t>(out) & 3) == 0;
-    for (int row = warp; row < k_valid * N; row += kThreads / 32) {
-        const int k = row / N, r = row - k * N;
-        const int *rp = acc + k * img_words + r * (N + 1);
-        unsigned vals[4];
-        unsigned local = 0;
-        for (int j = 0; j < cpl; ++j) {
-            int c = lane * cpl + j;
-            unsigned x = (c < N) ? (unsigned)rp[c] : 0u;
-            local += x;
-            vals[j] = local;
-        }
-        unsigned incl = local;
-        for (int o = 1; o < 32; o <<= 1) {
-            unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += t;
-        }
-        const unsigned excl = incl - local;
-        uint16_t *dst = out + (int64_t)img_idx[k] * npix + (int64_t)r * N;
-        if (pairs) {
-            for (int j = 0; j < cpl; j += 2) {
-                int c = lane * cpl + j;
-                if (c < N)
-                    *reinterpret_cast<unsigned *>(dst + c) =
-                        min(vals[j] + excl, 65535u) | (min(vals[j + 1] + excl, 65535u) << 16);
-            }
-        } else {
+    for (int k = 0; k < k_valid; ++k) {
+        for (int r = warp; r < N; r += kThreads / 32) {
+            const int *rp = acc + k * img_words + r * (N + 1);
+            unsigned vals[4];
+            unsigned local = 0;
             for (int j = 0; j < cpl; ++j) {
                 int c = lane * cpl + j;
-                if (c < N) dst[c] = (uint16_t)min(vals[j] + excl, 65535u);
+                unsigned x = (c < N) ? (unsigned)rp[c] : 0u;
+                local += x;
+                vals[j] = local;
+            }
+            unsigned incl = local;
+            for (int o = 1; o < 32; o <<= 1) {
+                unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            const unsigned excl = incl - local;
+            uint16_t *dst = out + (int64_t)img_idx[k] * npix + (int64_t)r * N;
+            if (pairs) {
+                for (int j = 0; j < cpl; j += 2) {
+                    int c = lane * cpl + j;
+                    if (c < N)
+                        *reinterpret_cast<unsigned *>(dst + c) =
+                            min(vals[j] + excl, 65535u) | (min(vals[j + 1] + excl, 65535u) << 16);
+                }
+            } else {
+                for (int j = 0; j < cpl; ++j) {
+                    int c = lane * cpl + j;
+                    if (c < N) dst[c] = (uint16_t)min(vals[j] + excl, 65535u);
+                }
             }
         }
     }
