@@ -121,10 +121,15 @@ RICI_API rici_status rici_crss_search(const uint16_t *needles, int64_t n_needles
 /* rici_crss_search with options.  flags:
  *   RICI_CRSS_SIMT        use the SIMT kernel even for n_bins = 64 (no synchronisation)
  *   RICI_CRSS_EARLY_EXIT  rank mode ("cease execution when a predetermined distance
- *                         threshold is exceeded"): a needle's accumulation over a group of 32
- *                         haystack images stops once every partial sum is >= t_i.  Partial
- *                         sums only grow, so the ranks are identical (G12); implies
- *                         RICI_CRSS_SIMT.  Needle entries are visited in decreasing |D_n|.  */
+ *                         threshold is exceeded").  Every CRSS term is a square, so the sum
+ *                         over any subset of pixels is a lower bound and stopping once it is
+ *                         >= t_i leaves the ranks identical (G12).
+ *                         Tensor path (n_bins = 64): two prune-check passes over the K prefixes
+ *                         of image rows 24-39 and 16-47 retire every 256 x 256 tile whose
+ *                         guard-valid pairs are all >= t_i; the survivors run the full K.
+ *                         With RICI_CRSS_SIMT: a needle's accumulation over a group of 32
+ *                         haystack images stops once every partial sum is >= t_i (needle
+ *                         entries visited in decreasing |D_n|).                             */
 #define RICI_CRSS_SIMT 1u
 #define RICI_CRSS_EARLY_EXIT 2u
 RICI_API rici_status rici_crss_search_ex(const uint16_t *needles, int64_t n_needles,

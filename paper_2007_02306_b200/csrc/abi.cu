@@ -151,12 +151,12 @@ bool valid_bins(int32_t n_bins) { return n_bins >= 2 && n_bins <= 128; }
 // thr_from_pairs: `thr` is an output, t_i = CRSS(n_i, h_i) (a10) -- the tensor path computes it
 // inside its feature pass, the SIMT path with the pair kernel first.
 cudaError_t count_below(const void *dn, int64_t nn, const void *dh, int64_t nh, int N, uint64_t *thr,
-                        bool thr_from_pairs, uint32_t *counts, cudaStream_t s) {
+                        bool thr_from_pairs, bool rank_mode, uint32_t *counts, cudaStream_t s) {
     // the tensor path streams 16-byte vectors of both image arrays
     const bool aligned = ((reinterpret_cast<uintptr_t>(dn) | reinterpret_cast<uintptr_t>(dh)) & 15) == 0;
     if (aligned && rici::use_mma_path(N)) {
         cudaError_t e = rici::launch_crss_count_mma((const uint16_t *)dn, nn, (const uint16_t *)dh, nh, thr,
-                                                    thr_from_pairs, counts, s);
+                                                    thr_from_pairs, rank_mode, counts, s);
         if (e != cudaErrorNotSupported) return e;
         cudaGetLastError();
     }
@@ -166,7 +166,7 @@ cudaError_t count_below(const void *dn, int64_t nn, const void *dh, int64_t nh, 
         if (e != cudaSuccess) return e;
     }
     return rici::launch_crss_search_tiles((const uint16_t *)dn, nn, (const uint16_t *)dh, nh, N, thr, counts,
-                                          nullptr, s);
+                                          nullptr, s, rank_mode);
 }
 
 rici_status check_images(const void *p, int64_t n, const char *name) {
@@ -366,7 +366,7 @@ rici_status rici_crss_count_below(const uint16_t *needles, int64_t n_needles,
     if (e == cudaSuccess) e = st.in(thresholds, sizeof(uint64_t) * (size_t)n_needles, &dt);
     if (e == cudaSuccess) e = st.out(out_counts, sizeof(uint32_t) * (size_t)n_needles, &dc);
     if (e == cudaSuccess) e = count_below(dn, n_needles, dh, n_haystack, n_bins, (uint64_t *)const_cast<void *>(dt),
-                                          false, (uint32_t *)dc, s);
+                                          false, false, (uint32_t *)dc, s);
     if (e == cudaSuccess) e = st.finish();
     if (e != cudaSuccess) return cuda_fail(e, "rici_crss_count_below");
     return RICI_OK;
@@ -424,9 +424,11 @@ rici_status rici_crss_search_ex(const uint16_t *needles, int64_t n_needles, cons
     if (e == cudaSuccess) e = cudaMallocAsync((void **)&thr, sizeof(uint64_t) * (size_t)n_needles, s);
     if (e == cudaSuccess) st.temps.push_back(thr);
     // a10: t_i = CRSS(n_i, h_i) ("this threshold can be trivially precomputed") -- by
-    // the pair kernel for the SIMT modes, inside count_below's feature pass otherwise
+    // the pair kernel for the SIMT path, inside count_below's feature pass otherwise.
+    // RICI_CRSS_EARLY_EXIT alone: rank mode on the best path (tensor tiles pruned by a K-prefix
+    // bound at N = 64); with RICI_CRSS_SIMT: the SIMT kernel's per-pair early exit.
     if (e == cudaSuccess) {
-        if (flags & (RICI_CRSS_SIMT | RICI_CRSS_EARLY_EXIT)) {
+        if (flags & RICI_CRSS_SIMT) {
             e = rici::launch_crss_pairs((const uint16_t *)dn, n_needles, (const uint16_t *)dh, n_haystack,
                                         n_bins, nullptr, n_needles, thr, s);
             if (e == cudaSuccess)
@@ -434,7 +436,8 @@ rici_status rici_crss_search_ex(const uint16_t *needles, int64_t n_needles, cons
                                                    n_bins, thr, (uint32_t *)dr, nullptr, s,
                                                    (flags & RICI_CRSS_EARLY_EXIT) != 0);
         } else {
-            e = count_below(dn, n_needles, dh, n_haystack, n_bins, thr, true, (uint32_t *)dr, s);
+            e = count_below(dn, n_needles, dh, n_haystack, n_bins, thr, true, (flags & RICI_CRSS_EARLY_EXIT) != 0,
+                            (uint32_t *)dr, s);
         }
     }
     if (e == cudaSuccess) e = st.finish();

@@ -57,9 +57,11 @@ cudaError_t launch_crss_search_tiles(const uint16_t *d_needles, int64_t nn,
 
 // a9-a12 on the tensor cores (N = 64): rank counts with the int8 tcgen05 GEMM formulation,
 // exact fallback to the SIMT kernel for images outside the int8 guard.
-// thr_from_pairs: d_thr is OUTPUT, t_i = CRSS(n_i, h_i) computed in the feature pass (nn <= nh)
+// thr_from_pairs: d_thr is OUTPUT, t_i = CRSS(n_i, h_i) computed in the feature pass (nn <= nh).
+// rank_mode: tiles whose pairs are all ruled out by a K-prefix lower bound skip the rest (f1).
 cudaError_t launch_crss_count_mma(const uint16_t *d_needles, int64_t nn, const uint16_t *d_haystack, int64_t nh,
-                                  uint64_t *d_thr, bool thr_from_pairs, uint32_t *d_counts, cudaStream_t s);
+                                  uint64_t *d_thr, bool thr_from_pairs, bool rank_mode, uint32_t *d_counts,
+                                  cudaStream_t s);
 
 // f4: Eq. 8 clutter fraction per oriented point (quadrature of the area inside the support
 // cylinder; object_tag [nt] in caller triangle order, device memory).

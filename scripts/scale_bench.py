@@ -2,7 +2,8 @@
   * construction of a clutterbox scene (C3-shaped: n objects, all scene vertices),
   * CRSS rank search, needles = the reference object alone, haystack = the scene (C4-shaped),
     in full mode on the tensor cores, full mode on the SIMT kernel, and rank mode with early
-    exit -- the three must give identical ranks.
+    exit on the tensor path (tile pruning by K-prefix bounds) and on the SIMT kernel --
+    all four must give identical ranks.
 Prints one JSON line."""
 import argparse
 import json
@@ -59,7 +60,8 @@ reps = 1 if a.c4 else 3
 r_mma, t_mma = timed(lambda: rici.rici_crss_search(nee, hay), reps)
 r_simt, t_simt = timed(lambda: rici.rici_crss_search(nee, hay, simt=True), reps)
 r_early, t_early = timed(lambda: rici.rici_crss_search(nee, hay, early_exit=True), reps)
-same = bool(torch.equal(r_mma, r_simt) and torch.equal(r_mma, r_early))
+r_es, t_es = timed(lambda: rici.rici_crss_search(nee, hay, early_exit=True, simt=True), reps)
+same = bool(torch.equal(r_mma, r_simt) and torch.equal(r_mma, r_early) and torch.equal(r_mma, r_es))
 r = r_mma.cpu().numpy()
 print(json.dumps({
     "scene": {"config": "C4" if a.c4 else "scaled", "objects": 10 if a.c4 else a.objects, "grid": [nu, nv],
@@ -68,6 +70,7 @@ print(json.dumps({
     "search": {"needles": int(nee.shape[0]), "haystack": int(hay.shape[0]), "comparisons": cmp,
                "full_tensor": {"ms": t_mma, "comparisons_per_s": cmp / t_mma * 1e3},
                "full_simt": {"ms": t_simt, "comparisons_per_s": cmp / t_simt * 1e3},
-               "rank_early_exit": {"ms": t_early, "comparisons_per_s": cmp / t_early * 1e3},
+               "rank_tensor_pruned": {"ms": t_early, "comparisons_per_s": cmp / t_early * 1e3},
+               "rank_simt_early_exit": {"ms": t_es, "comparisons_per_s": cmp / t_es * 1e3},
                "ranks_identical": same, "rank0_fraction": float((r == 0).mean()),
                "median_rank": float(np.median(r))}}))

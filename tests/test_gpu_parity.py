@@ -263,6 +263,42 @@ def test_crss_count_mma_guard_and_fallback(rici, oracle_mod, big):
     assert np.array_equal(r.astype(np.uint32), oracle_mod.ranks(A, H))
 
 
+def _band_copies(rng, A, rows, k):
+    """Copies of needle images whose changes differ from the original only in `rows`."""
+    out = A[rng.integers(0, A.shape[0], k)].copy()
+    for img in out:
+        r = rng.choice(rows)
+        img[r, rng.integers(1, 64):] += np.uint16(rng.integers(1, 4))
+    return out
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_rank_mode_tensor_pruning_exact(rici, oracle_mod, seed):
+    """Rank mode on the tensor path: tiles are retired after the K prefixes of rows 24-39 and
+    16-47 when every guard-valid pair's partial CRSS is already >= t_i.  The haystack mixes
+    pairs that are ruled out by the first prefix, only by the second, only by the full K
+    (differences outside rows 16-47), never (duplicates, ranks > 0), and guard-breaking
+    images -- the ranks must equal full mode and the oracle exactly."""
+    rng = np.random.default_rng(100 + seed)
+    A = _mixed_images(rng, 520, 6, 5, 200)                      # ragged: 520 needles (5 M tiles)
+    H = np.concatenate([
+        A + (rng.random(A.shape) < 0.002).astype(np.uint16),      # true matches, small t_i > 0
+        _band_copies(rng, A, list(range(24, 40)), 200),           # differ inside the first band
+        _band_copies(rng, A, list(range(16, 24)) + list(range(40, 48)), 200),   # second band only
+        _band_copies(rng, A, list(range(0, 16)) + list(range(48, 64)), 200),    # outside both
+        A[rng.integers(0, 520, 60)],                              # exact duplicates
+        _mixed_images(rng, 333, 6, 4, 40)])
+    H = np.ascontiguousarray(H)
+    full = rici.rici_crss_search(_dev(A), _dev(H)).cpu().numpy()
+    rank = rici.rici_crss_search(_dev(A), _dev(H), early_exit=True).cpu().numpy()
+    simt = rici.rici_crss_search(_dev(A), _dev(H), early_exit=True, simt=True).cpu().numpy()
+    ref = oracle_mod.ranks(A, H)
+    assert np.array_equal(full.astype(np.uint32), ref)
+    assert np.array_equal(rank.astype(np.uint32), ref)
+    assert np.array_equal(simt.astype(np.uint32), ref)
+    assert ref.max() > 0 and (ref == 0).any()
+
+
 def test_crss_paths_agree_subprocess(tmp_path):
     """The SIMT path (RICI_CRSS_PATH=simt) and the tensor-core path give identical ranks."""
     import os
