@@ -33,6 +33,26 @@ LANES_PER_SM = 128          # FP32/INT32 lanes per SM
 CRSS_OPS_PER_TERM = 3       # D_h difference, (D_n - D_h), multiply-accumulate
 
 
+def ncu_traffic(kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum of `kernel` per launch, from the newest
+    committed `ncu --set full` summary under profiles/ (r1*_ncu_summary.txt); None if absent."""
+    import glob
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_summary.txt")), reverse=True):
+        cur, tot, seen = None, 0.0, 0
+        for line in open(path):
+            if line.startswith("== "):
+                cur = line[3:].strip()
+            elif cur and cur.split("<")[0] == kernel and "dram__bytes_" in line:
+                parts = line.split("=")[1].split()
+                if len(parts) == 2 and parts[1] in scale:
+                    tot += float(parts[0]) * scale[parts[1]]
+                    seen += 1
+        if seen == 2:
+            return tot, os.path.relpath(path, ROOT) + " (cold-cache ncu replay, one launch)"
+    return None, None
+
+
 def peaks():
     try:
         with open(PEAKS_PATH) as f:
@@ -313,7 +333,7 @@ def run_gpu(args):
 
     # ---- roofline of the dominant kernel: the tcgen05 int8 GEMM that ranks all pairs
     # (DESIGN.md 6.2).  Algorithmic ops per comparison = 2 x K with K = 2 x 4096 int8 features;
-    # peak = the measured bf16 dense burst x 2 (nominal int8 : bf16 ratio on B200).
+    # peak = the nominal dense int8 4.5 POPS (the measured-derived figures ride along).
     pk, src = peaks()
     sm_mhz = pk.get("sm_max_mhz", 1965.0)
     imgs_np = imgs.cpu().numpy().view(np.uint16)
@@ -327,8 +347,10 @@ def run_gpu(args):
         derived = 2.0 * pk.get("bf16_tflops", 1587.6)              # measured bf16 x nominal ratio
         peak = 4500.0                                              # nominal dense int8 (guide table)
         arch = SMS * 8192 * 2 * sm_mhz * 1e6 / 1e12                # 8192 int8 MAC/clk/SM at sm_max
+        traffic, tsrc = ncu_traffic("crss_mma2_kernel")
         roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": None,
+                "frac": achieved / peak, "traffic": traffic,
+                "traffic_source": tsrc,
                 "kernel": "crss_mma2_kernel (tcgen05.mma.cta_group::2.kind::i8, TMA, TMEM) timed as the "
                           "whole rici_crss_search call (features, thresholds, fallback bookkeeping included)",
                 "dtype": "int8 x int8 -> int32",
@@ -350,8 +372,9 @@ def run_gpu(args):
         terms = float(nnz) * n
         achieved = terms * CRSS_OPS_PER_TERM / crss_s / 1e12
         peak = SMS * LANES_PER_SM * sm_mhz * 1e6 / 1e12
+        traffic, tsrc = ncu_traffic("crss_tile_kernel")
         roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s",
-                "frac": achieved / peak, "traffic": None,
+                "frac": achieved / peak, "traffic": traffic, "traffic_source": tsrc,
                 "kernel": "crss_tile_kernel (SIMT; timed as the rici_crss_search call)",
                 "peak_source": f"{SMS} SMs x {LANES_PER_SM} INT32 lanes x sm_max {sm_mhz} MHz ({src} clock)",
                 "algorithmic": f"{CRSS_OPS_PER_TERM} int ops per masked term; {nnz} masked needle terms "

@@ -22,13 +22,14 @@ WANT = ["gpu__time_duration.sum", "sm__throughput.avg.pct_of_peak_sustained_elap
 def main(path):
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
-    h = rows[0]
+    h, units = rows[0], rows[1]
     for r in rows[2:]:
         name = r[h.index("Kernel Name")].split("(")[0].split("::")[-1]
         print(f"== {name}")
         for w in WANT:
             if w in h:
-                print(f"   {w} = {r[h.index(w)]}")
+                u = units[h.index(w)]
+                print(f"   {w} = {r[h.index(w)]}" + (f" {u}" if u else ""))
 
 
 if __name__ == "__main__":

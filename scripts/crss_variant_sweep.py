@@ -1,0 +1,38 @@
+"""CRSS tuning sweep: throwaway builds with -D defines (RICI_NVCC_DEFINES), each timing
+rici_crss_search on the C2 self-search (images generated once per process)."""
+import json, os, shutil, subprocess, sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CODE = r'''
+import json, sys, torch, numpy as np
+sys.path.insert(0, sys.argv[1]); sys.path.insert(1, sys.argv[2])
+import synth, paper_2007_02306_b200 as rici
+cfg = synth.config_c2(); m = cfg["mesh"]
+mesh = rici.rici_create_mesh(torch.from_numpy(m.vertices).cuda(), torch.from_numpy(m.indices).cuda())
+imgs = rici.rici_generate(mesh, torch.from_numpy(cfg["origins"]).cuda(), 0.3, 64)
+flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+for _ in range(3): r = rici.rici_crss_search(imgs, imgs)
+ts = []
+for _ in range(10):
+    flush.fill_(1.0)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(); r = rici.rici_crss_search(imgs, imgs); b.record(); torch.cuda.synchronize()
+    ts.append(a.elapsed_time(b))
+print(json.dumps({"ms": float(np.median(ts)), "rank_sum": int(r.sum())}))
+'''
+variants = sys.argv[1:] or [""]
+dirs = {}
+for v in variants:
+    d = f"/tmp/rici_cvar_{abs(hash(v))}"
+    shutil.rmtree(d, ignore_errors=True)
+    shutil.copytree(os.path.join(ROOT, "paper_2007_02306_b200"), os.path.join(d, "paper_2007_02306_b200"))
+    shutil.copytree(os.path.join(ROOT, "include"), os.path.join(d, "include"))
+    r = subprocess.run([sys.executable, os.path.join(d, "paper_2007_02306_b200", "build.py"), "--force"],
+                       env=dict(os.environ, RICI_NVCC_DEFINES=v), capture_output=True, text=True)
+    if r.returncode:
+        print(v, "BUILD FAILED", r.stderr[-400:]); continue
+    dirs[v] = d
+for rnd in range(int(os.environ.get("ROUNDS", "2"))):
+    for v, d in dirs.items():
+        r = subprocess.run([sys.executable, "-c", CODE, d, ROOT], capture_output=True, text=True)
+        print(json.dumps({"round": rnd, "defines": v, "res": r.stdout.strip(), "err": r.stderr.strip()[-200:]}), flush=True)
