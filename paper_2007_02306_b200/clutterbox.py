@@ -2,7 +2,8 @@
 
 The protocol, step by step:
   1. a clutterbox of side s (default 3, P:425);
-  2. n objects (here seeded synthetic bumpy tori instead of SHREC2017, which is not available);
+  2. n objects drawn at random from an object set (here a pool of seeded synthetic bumpy tori
+     instead of SHREC2017, which is not available);
   3. each normalised to the unit sphere;
   4. the reference object is object 0;
   5. reference descriptors {RD}: one RICI per unique vertex of the reference object alone;
@@ -44,15 +45,30 @@ def rank_histogram(ranks: np.ndarray, n_haystack: int) -> dict:
             "rank0_fraction": float((r == 0).mean()) if r.size else 0.0}
 
 
-def build_scene_objects(scene: int, n_objects: int, grid=(120, 60)):
-    """Seeded synthetic objects for one scene (unit-sphere bumpy tori, varied minor radius)."""
+_POOL: dict = {}
+
+
+def object_pool(grid=(120, 60), size: int = 64):
+    """The object set scenes draw from (the paper draws from SHREC2017's 383 objects):
+    `size` seeded unit-sphere bumpy tori with varied minor radius, built once per grid."""
     import synth
-    objs = []
-    for k in range(n_objects):
-        rng = synth.rng_for(5, scene, k, 99)
-        objs.append(synth.bumpy_torus(grid[0], grid[1], key=(5, scene, k),
-                                      minor=float(rng.uniform(0.2, 0.45)), amp=0.08))
-    return objs
+    key = (tuple(grid), size)
+    if key not in _POOL:
+        objs = []
+        for k in range(size):
+            rng = synth.rng_for(5, k, 99)
+            objs.append(synth.bumpy_torus(grid[0], grid[1], key=(5, k),
+                                          minor=float(rng.uniform(0.2, 0.45)), amp=0.08))
+        _POOL[key] = objs
+    return _POOL[key]
+
+
+def build_scene_objects(scene: int, n_objects: int, grid=(120, 60), pool_size: int = 64):
+    """n distinct objects drawn at random (seeded per scene) from the object pool."""
+    import synth
+    pool = object_pool(grid, max(pool_size, n_objects))
+    pick = synth.rng_for(5, scene, 77).choice(len(pool), n_objects, replace=False)
+    return [pool[int(i)] for i in pick]
 
 
 def clutter_rank_heatmap(clutter: np.ndarray, ranks: np.ndarray, n_clutter_bins: int = 10,
