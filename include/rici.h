@@ -183,6 +183,21 @@ RICI_API const char *rici_last_error(void);
 /* Total number of kernels this library has launched in this process. */
 RICI_API uint64_t rici_launch_count(void);
 
+/* Per-kernel device timing (for the roofline: a kernel's own launch durations, measured live
+ * with CUDA events recorded on the stream each launch is issued to).  Off by default; while
+ * on, every launch of the timed kernels records an event pair (a few microseconds of host
+ * work, no device synchronisation).
+ *   kernel  RICI_KERNEL_GENERATE   the construction kernel of rici_generate
+ *           RICI_KERNEL_CRSS_MMA   the tcgen05 GEMM launch(es) of one count / search call
+ *                                  (rank mode: all its passes together)
+ * rici_kernel_time_ms waits for the recorded events, writes the mean duration in ms per
+ * recorded launch (0 if none) and the launch count, and clears the record.  Errors:
+ * RICI_ERR_INVALID_ARGUMENT for an unknown kernel id or NULL output.                    */
+#define RICI_KERNEL_GENERATE 0
+#define RICI_KERNEL_CRSS_MMA 1
+RICI_API rici_status rici_set_kernel_timing(int32_t enable);
+RICI_API rici_status rici_kernel_time_ms(int32_t kernel, float *out_mean_ms, int64_t *out_launches);
+
 /* "rici-b200 <version> sm_100a" */
 RICI_API const char *rici_version(void);
 

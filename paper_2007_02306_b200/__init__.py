@@ -20,7 +20,8 @@ from ._lib import RiciError, check, load
 
 __all__ = ["Mesh", "RiciError", "rici_create_mesh", "rici_destroy_mesh", "rici_generate",
            "rici_crss_search", "rici_crss_search_ex", "rici_clutter_fraction", "rici_crss_pairs", "rici_crss_count_below", "rici_crss_distances",
-           "rici_launch_count", "rici_version", "library_path"]
+           "rici_launch_count", "rici_set_kernel_timing", "rici_kernel_time_ms", "rici_version",
+           "library_path"]
 
 
 def library_path() -> str:
@@ -223,6 +224,19 @@ def rici_clutter_fraction(mesh: Mesh, object_tag, origins, support_radius: float
 
 def rici_launch_count() -> int:
     return int(load().rici_launch_count())
+
+
+def rici_set_kernel_timing(enable: bool) -> None:
+    """``rici_set_kernel_timing``: record CUDA events around the timed kernels' launches."""
+    check(load().rici_set_kernel_timing(1 if enable else 0))
+
+
+def rici_kernel_time_ms(kernel: int) -> tuple[float, int]:
+    """``rici_kernel_time_ms``: (mean ms per recorded launch, launches) of kernel id
+    RICI_KERNEL_GENERATE (0) or RICI_KERNEL_CRSS_MMA (1); clears the record."""
+    ms, n = ctypes.c_float(0.0), ctypes.c_int64(0)
+    check(load().rici_kernel_time_ms(int(kernel), ctypes.byref(ms), ctypes.byref(n)))
+    return float(ms.value), int(n.value)
 
 
 def rici_version() -> str:

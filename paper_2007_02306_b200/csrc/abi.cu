@@ -22,6 +22,34 @@ struct rici_mesh_s {
 namespace rici {
 static std::atomic<unsigned long long> g_launches{0};
 void note_launches(int k) { g_launches.fetch_add((unsigned long long)k, std::memory_order_relaxed); }
+
+// ---- per-kernel timing: event pairs recorded around launches, drained by rici_kernel_time_ms
+static std::atomic<int> g_timing{0};
+static std::mutex g_timing_mu;
+struct TimedLaunch { cudaEvent_t a, b; };
+static std::vector<TimedLaunch> g_timed[2];          // per kernel id: recorded pairs
+static std::vector<cudaEvent_t> g_event_pool;
+static cudaEvent_t g_open[2] = {nullptr, nullptr};  // begin event of the launch in flight
+static cudaEvent_t take_event() {
+    cudaEvent_t e = nullptr;
+    if (!g_event_pool.empty()) { e = g_event_pool.back(); g_event_pool.pop_back(); }
+    else cudaEventCreate(&e);
+    return e;
+}
+void timing_begin(int kernel, cudaStream_t s) {
+    if (!g_timing.load(std::memory_order_relaxed)) return;
+    std::lock_guard<std::mutex> lock(g_timing_mu);
+    cudaEvent_t e = take_event();
+    if (e && cudaEventRecord(e, s) == cudaSuccess) g_open[kernel] = e;
+}
+void timing_end(int kernel, cudaStream_t s) {
+    if (!g_timing.load(std::memory_order_relaxed)) return;
+    std::lock_guard<std::mutex> lock(g_timing_mu);
+    if (!g_open[kernel]) return;
+    cudaEvent_t e = take_event();
+    if (e && cudaEventRecord(e, s) == cudaSuccess) g_timed[kernel].push_back({g_open[kernel], e});
+    g_open[kernel] = nullptr;
+}
 cudaError_t ensure_smem(const void *kernel, size_t bytes) {
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
@@ -182,6 +210,36 @@ extern "C" {
 const char *rici_last_error(void) { return g_err.c_str(); }
 
 uint64_t rici_launch_count(void) { return rici::g_launches.load(); }
+
+rici_status rici_set_kernel_timing(int32_t enable) {
+    g_err.clear();
+    rici::g_timing.store(enable ? 1 : 0);
+    return RICI_OK;
+}
+
+rici_status rici_kernel_time_ms(int32_t kernel, float *out_mean_ms, int64_t *out_launches) {
+    g_err.clear();
+    if (kernel != RICI_KERNEL_GENERATE && kernel != RICI_KERNEL_CRSS_MMA)
+        return fail(RICI_ERR_INVALID_ARGUMENT, "unknown kernel id %d", (int)kernel);
+    if (!out_mean_ms || !out_launches) return fail(RICI_ERR_INVALID_ARGUMENT, "null output");
+    std::lock_guard<std::mutex> lock(rici::g_timing_mu);
+    double sum = 0.0;
+    int64_t cnt = 0;
+    cudaError_t err = cudaSuccess;
+    for (auto &t : rici::g_timed[kernel]) {
+        float ms = 0.f;
+        cudaError_t e = cudaEventSynchronize(t.b);
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, t.a, t.b);
+        if (e == cudaSuccess) { sum += ms; ++cnt; } else if (err == cudaSuccess) err = e;
+        rici::g_event_pool.push_back(t.a);
+        rici::g_event_pool.push_back(t.b);
+    }
+    rici::g_timed[kernel].clear();
+    *out_mean_ms = cnt ? (float)(sum / (double)cnt) : 0.f;
+    *out_launches = cnt;
+    if (err != cudaSuccess) return cuda_fail(err, "rici_kernel_time_ms");
+    return RICI_OK;
+}
 
 const char *rici_version(void) { return "rici-b200 0.1.0 sm_100a"; }
 

@@ -28,6 +28,10 @@ cudaError_t spatial_order(const float *d_pts, int stride, int64_t n, int *d_perm
 
 // Kernel-launch bookkeeping (rici_launch_count()).
 void note_launches(int k);
+// Per-kernel event timing (rici_set_kernel_timing): begin/end bracket the kernel's launch(es)
+// on stream s; no-ops while timing is off.
+void timing_begin(int kernel, cudaStream_t s);
+void timing_end(int kernel, cudaStream_t s);
 
 // Raises a kernel's dynamic shared-memory limit to `bytes` on the current device (once per
 // (kernel, device); thread-safe).

@@ -18,8 +18,13 @@ def gen(mesh):
 ref, sc = gen(cfg["reference"]), gen(cfg["scene"])
 nn, nh = ref.shape[0], sc.shape[0]
 tiles = [int(x) for x in np.linspace(0, nn // 256 - 1, 6)]
+def pairs(js):
+    return [r for j in js for r in (2 * j, 2 * j + 1)]
 subsets = {"all": list(range(64)), "mid16": list(range(24, 40)), "mid32": list(range(16, 48)),
-           "lo16": list(range(0, 16))}
+           "lo16": list(range(0, 16)),
+           "spread16": pairs(range(1, 32, 4)), "spread16b": pairs(range(2, 32, 4)),
+           "midspread16": pairs([8, 10, 12, 14, 17, 19, 21, 23]),
+           "spread32": pairs(range(0, 32, 2)), "mid8": list(range(28, 36)), "spread8": pairs(range(2, 32, 8))}
 res = {"nn": nn, "nh": nh, "tiles": tiles, "frac_prunable": {k: [] for k in subsets}}
 for t0 in tiles:
     nd = ref[t0 * 256:(t0 + 1) * 256].contiguous()

@@ -26,13 +26,23 @@ def _declared():
 
 def test_header_symbols_exported(lib):
     declared = _declared()
-    assert len(declared) == 13
+    assert len(declared) == 15
     out = subprocess.run(["nm", "-D", "--defined-only", os.path.join(ROOT, "paper_2007_02306_b200", "librici.so")],
                          capture_output=True, text=True, check=True).stdout
     exported = set(re.findall(r" T (rici_\w+)", out))
     assert set(declared) <= exported
     for name in declared:
         assert hasattr(lib, name)
+
+
+def test_kernel_timing_api(lib):
+    import ctypes
+    ms, n = ctypes.c_float(1.0), ctypes.c_int64(7)
+    assert lib.rici_kernel_time_ms(5, ctypes.byref(ms), ctypes.byref(n)) == 1        # unknown id
+    assert lib.rici_kernel_time_ms(0, None, None) == 1                               # null outputs
+    assert lib.rici_kernel_time_ms(1, ctypes.byref(ms), ctypes.byref(n)) == 0
+    assert n.value == 0 and ms.value == 0.0                                          # nothing recorded
+    assert lib.rici_set_kernel_timing(0) == 0
 
 
 def test_sass_is_sm100a():
