@@ -27,8 +27,11 @@ for v in variants:
     shutil.rmtree(d, ignore_errors=True)
     shutil.copytree(os.path.join(ROOT, "paper_2007_02306_b200"), os.path.join(d, "paper_2007_02306_b200"))
     shutil.copytree(os.path.join(ROOT, "include"), os.path.join(d, "include"))
+    defines, _, src = v.partition("@")        # "DEFINES@file.cu": file.cu replaces crss_mma.cu
+    if src:
+        shutil.copy(os.path.join(ROOT, src), os.path.join(d, "paper_2007_02306_b200", "csrc", "crss_mma.cu"))
     r = subprocess.run([sys.executable, os.path.join(d, "paper_2007_02306_b200", "build.py"), "--force"],
-                       env=dict(os.environ, RICI_NVCC_DEFINES=v), capture_output=True, text=True)
+                       env=dict(os.environ, RICI_NVCC_DEFINES=defines), capture_output=True, text=True)
     if r.returncode:
         print(v, "BUILD FAILED", r.stderr[-400:]); continue
     dirs[v] = d
