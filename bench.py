@@ -389,6 +389,30 @@ def run_gpu(args):
                 "algorithmic": f"{CRSS_OPS_PER_TERM} int ops per masked term; {nnz} masked needle terms "
                                f"x {n} haystack images per rank"}
     roof["hbm_equivalent_frac"] = comparisons * 8192 / crss_s / 1e9 / pk.get("hbm_gbs", 6548.8)
+    # the north star's own CRSS design (warp-cooperative integer streaming compare over the
+    # needle change lists, ballot/popc rank) on the same images, outside the step
+    simt_line = None
+    if world == 1 and mma and not args.no_cpu_baseline:
+        ts = []
+        for it in range(3):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            flush.zero_()
+            a.record(stream)
+            r_simt = rici.rici_crss_search(imgs, imgs, simt=True)
+            b.record(stream)
+            torch.cuda.synchronize()
+            if it:
+                ts.append(a.elapsed_time(b))
+        d = np.diff(imgs_np.astype(np.int32), axis=2)
+        terms = float(int((d != 0).sum())) * n
+        t_s = float(np.mean(ts)) / 1e3
+        simt_line = {"ms": t_s * 1e3, "comparisons_per_s": comparisons / t_s,
+                     "ranks_equal_tensor_path": bool(torch.equal(r_simt.cpu(), ranks_d.cpu())),
+                     "roofline": {"bound": "alu", "achieved": terms * CRSS_OPS_PER_TERM / t_s / 1e12,
+                                  "peak": SMS * LANES_PER_SM * sm_mhz * 1e6 / 1e12, "unit": "Tops/s",
+                                  "frac": terms * CRSS_OPS_PER_TERM / t_s / (SMS * LANES_PER_SM * sm_mhz * 1e6),
+                                  "algorithmic": f"{CRSS_OPS_PER_TERM} int ops per masked needle term"},
+                     "note": "rici_crss_search(simt=True), whole call, not part of the timed step"}
     images_per_s = n_total_hay / (step_ms_max / 1e3)
     spp = segments_per_pair(cfg)
     alu_peak = SMS * LANES_PER_SM * sm_mhz * 1e6 / 1e12
@@ -413,6 +437,7 @@ def run_gpu(args):
             "comparisons_per_s": comparisons * world / (step_ms_max / 1e3),
             "construction": construction,
             "crss": {"ms": crss_ms, "comparisons_per_s": comparisons / crss_s},
+            "crss_simt_path": simt_line,
             "roofline": roof, "cpu_baseline": cb, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk.summary(), "bench_wall_s": wall}
     print(json.dumps(line))
