@@ -479,3 +479,28 @@ def test_unaligned_image_buffers(rici, oracle_mod):
     assert np.array_equal(rici.rici_crss_search(nv, hv).cpu().numpy().astype(np.uint32), oracle_mod.ranks(A, H))
     d = rici.rici_crss_distances(nv, hv).cpu().numpy().view(np.uint64)
     assert np.array_equal(d, oracle_mod.crss_matrix(A, H))
+
+
+def test_kernel_timing_api(rici):
+    """rici_set_kernel_timing / rici_kernel_time_ms: one event pair per launch of the timed
+    kernels, on the launch stream; durations positive; the record clears on read."""
+    cfg = synth.config_c1()
+    m = cfg["mesh"]
+    mesh = rici.rici_create_mesh(torch.from_numpy(m.vertices).to(DEV), torch.from_numpy(m.indices).to(DEV))
+    o = torch.from_numpy(cfg["origins"]).to(DEV)
+    rici.rici_kernel_time_ms(0), rici.rici_kernel_time_ms(1)
+    rici.rici_set_kernel_timing(True)
+    try:
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            imgs = [rici.rici_generate(mesh, o, cfg["R"], cfg["N"]) for _ in range(3)]
+            rici.rici_crss_search(imgs[0], imgs[1])                # N = 64: one GEMM launch
+    finally:
+        rici.rici_set_kernel_timing(False)
+    g_ms, g_n = rici.rici_kernel_time_ms(0)
+    c_ms, c_n = rici.rici_kernel_time_ms(1)
+    assert g_n == 3 and g_ms > 0 and c_n == 1 and c_ms > 0
+    assert rici.rici_kernel_time_ms(0) == (0.0, 0)
+    rici.rici_generate(mesh, o, cfg["R"], cfg["N"])                 # timing off: nothing recorded
+    assert rici.rici_kernel_time_ms(0) == (0.0, 0)
+    mesh.destroy()
