@@ -53,6 +53,19 @@ def ncu_traffic(kernel):
     return None, None
 
 
+def ncu_metric(kernel, metric):
+    """A metric of `kernel` from the newest committed ncu summary (profiles/r*_ncu_summary.txt)."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_summary.txt")), reverse=True):
+        cur = None
+        for line in open(path):
+            if line.startswith("== "):
+                cur = line[3:].strip()
+            elif cur and cur.split("<")[0] == kernel and line.strip().startswith(metric + " ="):
+                return float(line.split("=")[1].split()[0]), os.path.relpath(path, ROOT)
+    return None, None
+
+
 def peaks():
     try:
         with open(PEAKS_PATH) as f:
@@ -423,6 +436,10 @@ def run_gpu(args):
                     "paper_literal_frac": W / (gen_ms / 1e3) / (alu_peak * 1e12),
                     "note": "W = 43 P + 40 S + 3 N^2 n (brute-force pairs); the exact cull skips "
                             "provably-zero pairs, so this fraction can exceed 1"}
+    issue, isrc = ncu_metric("generate_kernel", "smsp__issue_active.avg.pct_of_peak_sustained_active")
+    if issue is not None:
+        construction["issue_slot_utilisation"] = issue / 100.0
+        construction["issue_source"] = isrc + " (ncu --set full; the kernel is issue-bound)"
     cb = cpu_baseline(cfg) if world == 1 and not args.no_cpu_baseline else None
     line = {"metric": METRIC, "value": images_per_s, "unit": "images/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms_max,
