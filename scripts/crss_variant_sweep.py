@@ -6,17 +6,25 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CODE = r'''
 import json, sys, torch, numpy as np
 sys.path.insert(0, sys.argv[1]); sys.path.insert(1, sys.argv[2])
+import os
 import synth, paper_2007_02306_b200 as rici
-cfg = synth.config_c2(); m = cfg["mesh"]
-mesh = rici.rici_create_mesh(torch.from_numpy(m.vertices).cuda(), torch.from_numpy(m.indices).cuda())
-imgs = rici.rici_generate(mesh, torch.from_numpy(cfg["origins"]).cuda(), 0.3, 64)
+def gen(m, o):
+    mesh = rici.rici_create_mesh(torch.from_numpy(m.vertices).cuda(), torch.from_numpy(m.indices).cuda())
+    return rici.rici_generate(mesh, torch.from_numpy(o).cuda(), 0.3, 64)
+if os.environ.get("WORKLOAD") == "c4":
+    c4 = synth.config_c4()
+    nee, hay = gen(c4["reference"], c4["reference"].origins), gen(c4["scene"], c4["scene"].origins)
+else:
+    cfg = synth.config_c2()
+    nee = hay = gen(cfg["mesh"], cfg["origins"])
+early = os.environ.get("RANK_MODE") == "1"
 flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
-for _ in range(3): r = rici.rici_crss_search(imgs, imgs)
+for _ in range(2): r = rici.rici_crss_search(nee, hay, early_exit=early)
 ts = []
-for _ in range(10):
+for _ in range(int(os.environ.get("REPS", "10"))):
     flush.fill_(1.0)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(); r = rici.rici_crss_search(imgs, imgs); b.record(); torch.cuda.synchronize()
+    a.record(); r = rici.rici_crss_search(nee, hay, early_exit=early); b.record(); torch.cuda.synchronize()
     ts.append(a.elapsed_time(b))
 print(json.dumps({"ms": float(np.median(ts)), "rank_sum": int(r.sum())}))
 '''
