@@ -300,7 +300,8 @@ def test_rank_mode_tensor_pruning_exact(rici, oracle_mod, seed):
 
 
 def test_crss_paths_agree_subprocess(tmp_path):
-    """The SIMT path (RICI_CRSS_PATH=simt) and the tensor-core path give identical ranks."""
+    """The SIMT path (RICI_CRSS_PATH=simt) and the three tensor-core kernels (RICI_MMA_MODE 0:
+    1-CTA, 1: 2-CTA multicast, 2: cta_group::2) give identical ranks and counts."""
     import os
     import subprocess
     import sys
@@ -312,14 +313,20 @@ def test_crss_paths_agree_subprocess(tmp_path):
         "mesh = r.rici_create_mesh(torch.from_numpy(m.vertices).cuda(), torch.from_numpy(m.indices).cuda())\n"
         "im = r.rici_generate(mesh, torch.from_numpy(m.origins).cuda(), 0.3, 64)\n"
         "ranks = r.rici_crss_search(im[:2000], im).cpu().numpy()\n"
-        "np.save(sys.argv[1], ranks)\n") % root
+        "pr = torch.stack([torch.arange(2000), (torch.arange(2000) * 7919) %% im.shape[0]], 1).cuda()\n"
+        "thr = r.rici_crss_pairs(im[:2000], im, pr)\n"
+        "cnt = r.rici_crss_count_below(im[:2000], im, thr).cpu().numpy()\n"
+        "np.save(sys.argv[1], np.concatenate([ranks.astype(np.int64), cnt.astype(np.int64)]))\n") % root
     outs = {}
-    for path in ("simt", "mma"):
-        env = dict(os.environ, RICI_CRSS_PATH=path)
-        f = str(tmp_path / f"{path}.npy")
+    for path, mode in (("simt", "2"), ("mma", "0"), ("mma", "1"), ("mma", "2")):
+        env = dict(os.environ, RICI_CRSS_PATH=path, RICI_MMA_MODE=mode)
+        f = str(tmp_path / f"{path}{mode}.npy")
         subprocess.run([sys.executable, "-c", code, f], env=env, check=True, timeout=600)
-        outs[path] = np.load(f)
-    assert np.array_equal(outs["simt"], outs["mma"])
+        outs[path + mode] = np.load(f)
+    ref = outs.pop("simt2")
+    assert ref[2000:].max() > 0                              # the counts are not trivially zero
+    for k, v in outs.items():
+        assert np.array_equal(ref, v), k
 
 
 def _mini_c4(n_clutter=4, grid=(60, 30)):
