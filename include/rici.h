@@ -77,8 +77,10 @@ RICI_API rici_status rici_create_mesh(const float *vertices, int64_t n_vertices,
                              const int32_t *indices, int64_t n_triangles,
                              rici_stream_t stream, rici_mesh *out_mesh);
 
-/* Frees the mesh: stream-ordered release on the legacy default stream, i.e. after all
- * previously enqueued work on blocking streams; does not block the host.  NULL is a no-op. */
+/* Frees the mesh: stream-ordered release on the legacy default stream, made to wait for the
+ * last rici_generate / rici_clutter_fraction that read the mesh on every stream it was used on
+ * (blocking or non-blocking); does not block the host.  The handle is invalid afterwards.
+ * NULL is a no-op. */
 RICI_API rici_status rici_destroy_mesh(rici_mesh mesh);
 
 /* Number of triangles in the mesh, or -1 for NULL. */

@@ -17,6 +17,21 @@
 
 struct rici_mesh_s {
     rici::DeviceMesh m;
+    // one event per stream the mesh was read on, recorded after each use: rici_destroy_mesh
+    // orders the frees after every recorded use, whatever the streams' flags
+    std::mutex mu;
+    std::vector<std::pair<cudaStream_t, cudaEvent_t>> uses;
+    void note_use(cudaStream_t s) {
+        std::lock_guard<std::mutex> lock(mu);
+        cudaEvent_t ev = nullptr;
+        for (auto &u : uses)
+            if (u.first == s) ev = u.second;
+        if (!ev) {
+            if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) { cudaGetLastError(); return; }
+            uses.emplace_back(s, ev);
+        }
+        cudaEventRecord(ev, s);
+    }
 };
 
 namespace rici {
@@ -303,8 +318,12 @@ rici_status rici_create_mesh(const float *vertices, int64_t n_vertices, const in
 rici_status rici_destroy_mesh(rici_mesh mesh) {
     g_err.clear();
     if (!mesh) return RICI_OK;
-    // ordered after all prior work on the legacy default stream (which every blocking stream,
-    // including the creation stream, synchronises with)
+    // stream-ordered frees on the legacy default stream, made to wait for the last recorded use
+    // on every stream the mesh was read on (non-blocking streams included); no host wait
+    for (auto &u : mesh->uses) {
+        cudaStreamWaitEvent(0, u.second, 0);
+        cudaEventDestroy(u.second);
+    }
     if (mesh->m.tri) cudaFreeAsync(mesh->m.tri, 0);
     if (mesh->m.sphere) cudaFreeAsync(mesh->m.sphere, 0);
     if (mesh->m.super_sphere) cudaFreeAsync(mesh->m.super_sphere, 0);
@@ -334,6 +353,7 @@ rici_status rici_generate(rici_mesh mesh, const float *origins, int64_t n, float
     if (e == cudaSuccess)
         e = rici::launch_generate(mesh->m, (const float *)dorig, n, support_radius, n_bins,
                                   (uint16_t *)dout, s);
+    if (e == cudaSuccess) mesh->note_use(s);
     if (e == cudaSuccess) e = st.finish();
     if (e != cudaSuccess) return cuda_fail(e, "rici_generate");
     return RICI_OK;
@@ -363,6 +383,7 @@ rici_status rici_clutter_fraction(rici_mesh mesh, const uint8_t *object_tag, con
     if (e == cudaSuccess)
         e = rici::launch_clutter_fraction(mesh->m, (const unsigned char *)dt, (const float *)dorig, n, support_radius,
                                           quadrature_q, (float *)df, (float *)da, s);
+    if (e == cudaSuccess) mesh->note_use(s);
     if (e == cudaSuccess) e = st.finish();
     if (e != cudaSuccess) return cuda_fail(e, "rici_clutter_fraction");
     return RICI_OK;

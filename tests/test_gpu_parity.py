@@ -511,3 +511,31 @@ def test_kernel_timing_api(rici):
     rici.rici_generate(mesh, o, cfg["R"], cfg["N"])                 # timing off: nothing recorded
     assert rici.rici_kernel_time_ms(0) == (0.0, 0)
     mesh.destroy()
+
+
+def test_destroy_mesh_ordered_after_nonblocking_stream_use(rici):
+    """rici_destroy_mesh right after an enqueued rici_generate on a non-blocking stream: the
+    frees wait for that use (event recorded by the library), so memory the pool hands to a new
+    mesh on another stream cannot be overwritten while the first generate still reads it."""
+    cfg = synth.config_c2()
+    m = cfg["mesh"]
+    o = torch.from_numpy(cfg["origins"]).to(DEV)
+    v, t = torch.from_numpy(m.vertices).to(DEV), torch.from_numpy(m.indices).to(DEV)
+    ref_mesh = rici.rici_create_mesh(v, t)
+    ref = rici.rici_generate(ref_mesh, o, 0.3, 64)
+    torch.cuda.synchronize()
+    ref_mesh.destroy()
+    junk_v = torch.rand_like(v) * 10 - 5                        # a different mesh of the same size
+    st = torch.cuda.Stream()                                     # torch streams are non-blocking
+    outs = []
+    for _ in range(3):
+        with torch.cuda.stream(st):
+            mesh = rici.rici_create_mesh(v, t, stream=st)
+            out = rici.rici_generate(mesh, o, 0.3, 64, stream=st)
+            mesh.destroy()                                       # no host wait before the free
+        junk = rici.rici_create_mesh(junk_v, t)                  # may reuse the freed blocks
+        junk.destroy()
+        outs.append(out)
+    torch.cuda.synchronize()
+    for out in outs:
+        assert torch.equal(out, ref)
