@@ -192,8 +192,9 @@ RICI_API uint64_t rici_launch_count(void);
  *   kernel  RICI_KERNEL_GENERATE   the construction kernel of rici_generate
  *           RICI_KERNEL_CRSS_MMA   the tcgen05 GEMM launch(es) of one count / search call
  *                                  (rank mode: all its passes together)
- * rici_kernel_time_ms waits for the recorded events, writes the mean duration in ms per
- * recorded launch (0 if none) and the launch count, and clears the record.  Errors:
+ * rici_kernel_time_ms waits for the recorded events, writes the mean device time in ms per
+ * API call (the durations of all of that call's timed launches summed; 0 if none) and the
+ * number of recorded launches, and clears the record.  Errors:
  * RICI_ERR_INVALID_ARGUMENT for an unknown kernel id or NULL output.                    */
 #define RICI_KERNEL_GENERATE 0
 #define RICI_KERNEL_CRSS_MMA 1

@@ -45,6 +45,7 @@ struct TimedLaunch { cudaEvent_t a, b; };
 static std::vector<TimedLaunch> g_timed[2];          // per kernel id: recorded pairs
 static std::vector<cudaEvent_t> g_event_pool;
 static cudaEvent_t g_open[2] = {nullptr, nullptr};  // begin event of the launch in flight
+static int64_t g_calls[2] = {0, 0};                  // API calls that recorded launches
 static cudaEvent_t take_event() {
     cudaEvent_t e = nullptr;
     if (!g_event_pool.empty()) { e = g_event_pool.back(); g_event_pool.pop_back(); }
@@ -56,6 +57,11 @@ void timing_begin(int kernel, cudaStream_t s) {
     std::lock_guard<std::mutex> lock(g_timing_mu);
     cudaEvent_t e = take_event();
     if (e && cudaEventRecord(e, s) == cudaSuccess) g_open[kernel] = e;
+}
+void timing_call(int kernel) {
+    if (!g_timing.load(std::memory_order_relaxed)) return;
+    std::lock_guard<std::mutex> lock(g_timing_mu);
+    ++g_calls[kernel];
 }
 void timing_end(int kernel, cudaStream_t s) {
     if (!g_timing.load(std::memory_order_relaxed)) return;
@@ -250,7 +256,9 @@ rici_status rici_kernel_time_ms(int32_t kernel, float *out_mean_ms, int64_t *out
         rici::g_event_pool.push_back(t.b);
     }
     rici::g_timed[kernel].clear();
-    *out_mean_ms = cnt ? (float)(sum / (double)cnt) : 0.f;
+    const int64_t calls = rici::g_calls[kernel];
+    rici::g_calls[kernel] = 0;
+    *out_mean_ms = calls ? (float)(sum / (double)calls) : 0.f;
     *out_launches = cnt;
     if (err != cudaSuccess) return cuda_fail(err, "rici_kernel_time_ms");
     return RICI_OK;

@@ -481,6 +481,7 @@ cudaError_t launch_generate(const DeviceMesh &m, const float *d_origins, int64_t
 #define RICI_GEN_LAUNCH(KK)                                                                             \
     generate_kernel<KK><<<(unsigned)blocks, kThreads, smem, s>>>(m.tri, m.sphere, m.n_chunks, m.super_sphere, \
                                                                  m.n_super, d_origins, perm, n, R, N, g, d_out)
+    timing_call(0);
     timing_begin(0, s);
     if (Kt == 8) RICI_GEN_LAUNCH(8);
     else if (Kt == 4) RICI_GEN_LAUNCH(4);

@@ -32,6 +32,7 @@ void note_launches(int k);
 // on stream s; no-ops while timing is off.
 void timing_begin(int kernel, cudaStream_t s);
 void timing_end(int kernel, cudaStream_t s);
+void timing_call(int kernel);            // once per API call: the mean is per call
 
 // Raises a kernel's dynamic shared-memory limit to `bytes` on the current device (once per
 // (kernel, device); thread-safe).

@@ -300,8 +300,9 @@ def test_rank_mode_tensor_pruning_exact(rici, oracle_mod, seed):
 
 
 def test_crss_paths_agree_subprocess(tmp_path):
-    """The SIMT path (RICI_CRSS_PATH=simt) and the three tensor-core kernels (RICI_MMA_MODE 0:
-    1-CTA, 1: 2-CTA multicast, 2: cta_group::2) give identical ranks and counts."""
+    """The SIMT path (RICI_CRSS_PATH=simt) and the four tensor-core kernels (RICI_MMA_MODE 0:
+    1-CTA, 1: 2-CTA multicast, 2: cta_group::2, 3: cta_group::2 with 2:4-sparse needle rows)
+    give identical ranks and counts."""
     import os
     import subprocess
     import sys
@@ -318,7 +319,7 @@ def test_crss_paths_agree_subprocess(tmp_path):
         "cnt = r.rici_crss_count_below(im[:2000], im, thr).cpu().numpy()\n"
         "np.save(sys.argv[1], np.concatenate([ranks.astype(np.int64), cnt.astype(np.int64)]))\n") % root
     outs = {}
-    for path, mode in (("simt", "2"), ("mma", "0"), ("mma", "1"), ("mma", "2")):
+    for path, mode in (("simt", "2"), ("mma", "0"), ("mma", "1"), ("mma", "2"), ("mma", "3")):
         env = dict(os.environ, RICI_CRSS_PATH=path, RICI_MMA_MODE=mode)
         f = str(tmp_path / f"{path}{mode}.npy")
         subprocess.run([sys.executable, "-c", code, f], env=env, check=True, timeout=600)
