@@ -361,27 +361,45 @@ def run_gpu(args):
     n_total_hay = n * world
     crss_s = crss_ms / 1e3
     mma = os.environ.get("RICI_CRSS_PATH", "") != "simt"
+    sparse = mma and os.environ.get("RICI_MMA_MODE", "3") == "3"
     if mma and n_mma_k > 0:
         K = 2 * 4096
-        kern_s = mma_kernel_ms / 1e3                               # the GEMM launch alone, live events
-        achieved = comparisons * 2.0 * K / kern_s / 1e12          # Tops/s (int8)
+        kern_s = mma_kernel_ms / 1e3                               # the GEMM launches, live events
+        achieved = comparisons * 2.0 * K / kern_s / 1e12          # logical int8 ops/s (Tops/s)
         derived = 2.0 * pk.get("bf16_tflops", 1587.6)              # measured bf16 x nominal ratio
-        peak = 4500.0                                              # nominal dense int8 (guide table)
         arch = SMS * 8192 * 2 * sm_mhz * 1e6 / 1e12                # 8192 int8 MAC/clk/SM at sm_max
-        traffic, tsrc = ncu_traffic("crss_mma2_kernel")
+        sp_rate = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "int8_sparse_rate.json")) as f:
+                sp_rate = json.load(f)["sparse"]["logical_tops"]
+        except Exception:
+            pass
+        if sparse:   # 2:4-sparse needle operand: NVIDIA's doubled (sparse) figure is the ceiling
+            peak = 9000.0
+            kname = ("crss_mma_sp_kernel (tcgen05.mma.sp.cta_group::2.kind::i8, 2:4 needle rows, 4-CTA clusters "
+                     "with B multicast) + the dense subset pass on a side stream")
+        else:
+            peak = 4500.0                                          # nominal dense int8 (guide table)
+            kname = "crss_mma2_kernel (tcgen05.mma.cta_group::2.kind::i8, TMA, TMEM)"
+        traffic, tsrc = ncu_traffic("crss_mma_sp_kernel" if sparse else "crss_mma2_kernel")
         roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": traffic,
                 "traffic_source": tsrc,
-                "kernel": "crss_mma2_kernel (tcgen05.mma.cta_group::2.kind::i8, TMA, TMEM)",
+                "kernel": kname,
                 "kernel_ms": mma_kernel_ms, "kernel_launches_timed": n_mma_k,
                 "timing": "CUDA events recorded by the library on the launch stream around each GEMM launch "
                           "in the timed region (rici_set_kernel_timing / rici_kernel_time_ms)",
                 "frac_of_whole_search_call": comparisons * 2.0 * K / crss_s / 1e12 / peak,
-                "dtype": "int8 x int8 -> int32",
-                "peak_source": "nominal dense int8 4.5 POPS (B200_PROFILING.md table).  The measured-derived "
-                               f"figure (bf16 dense burst {pk.get('bf16_tflops', 1587.6)} x 2 = {derived:.0f}) and "
-                               "cuBLAS int8 (profiles/int8_peak.json) are power-limited on random operands and "
-                               "read below this kernel, whose feature bytes are ~95% zero",
+                "dtype": "int8 (2:4-sparse needle rows) x int8 -> int32" if sparse else "int8 x int8 -> int32",
+                "peak_source": ("nominal 2:4-sparse int8 9 POPS (2 x the dense 4.5 POPS of B200_PROFILING.md, whose "
+                                "doubled vendor figures are the 2:4 ones); the measured sparse issue rate is "
+                                "profiles/int8_sparse_rate.json" if sparse else
+                                "nominal dense int8 4.5 POPS (B200_PROFILING.md table)") +
+                               f".  The measured-derived dense figure (bf16 dense burst {pk.get('bf16_tflops', 1587.6)}"
+                               f" x 2 = {derived:.0f}) and cuBLAS int8 (profiles/int8_peak.json) are power-limited on "
+                               "random operands",
+                "frac_vs_measured_sparse_rate": (achieved / sp_rate) if (sparse and sp_rate) else None,
+                "dense_equivalent_frac_of_dense_peak": achieved / 4500.0,
                 "frac_vs_measured_derived": achieved / derived,
                 "frac_vs_arch_at_sm_max": achieved / arch,
                 "algorithmic": f"2 x {K} int8 MACs per comparison x {comparisons:.0f} comparisons"}

@@ -21,12 +21,16 @@ early = os.environ.get("RANK_MODE") == "1"
 flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
 for _ in range(2): r = rici.rici_crss_search(nee, hay, early_exit=early)
 ts = []
+rici.rici_kernel_time_ms(1)
+rici.rici_set_kernel_timing(True)
 for _ in range(int(os.environ.get("REPS", "10"))):
     flush.fill_(1.0)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(); r = rici.rici_crss_search(nee, hay, early_exit=early); b.record(); torch.cuda.synchronize()
     ts.append(a.elapsed_time(b))
-print(json.dumps({"ms": float(np.median(ts)), "rank_sum": int(r.sum())}))
+rici.rici_set_kernel_timing(False)
+km, kn = rici.rici_kernel_time_ms(1)
+print(json.dumps({"ms": float(np.median(ts)), "gemm_ms": km, "rank_sum": int(r.sum())}))
 '''
 variants = sys.argv[1:] or [""]
 dirs = {}
