@@ -540,3 +540,23 @@ def test_destroy_mesh_ordered_after_nonblocking_stream_use(rici):
     torch.cuda.synchronize()
     for out in outs:
         assert torch.equal(out, ref)
+
+
+def test_sparse_needle_path_mixed(rici, oracle_mod):
+    """2:4-sparse tensor path (default RICI_MMA_MODE=3): sparse needle rows (D_n density ~2-3%,
+    like the RICI workloads) mixed with rows that break the 2:4 structure (counted by the dense
+    pass on the side stream) and rows that break the int8 guard (SIMT) -- 700 needles (6 M
+    tiles, 4-CTA clusters with a ragged last cluster) against 1,300 haystack images; counts and
+    ranks must equal the oracle."""
+    rng = np.random.default_rng(77)
+    A = _rand_imgs(rng, 700, hi=4, density=0.03)
+    dense_rows = rng.choice(700, 60, replace=False)
+    A[dense_rows] = _rand_imgs(rng, 60, hi=6, density=0.5)           # many > 2 per group: dense pass
+    A[rng.choice(700, 5, replace=False), 10, 20] = 300               # guard break: SIMT
+    H = np.concatenate([A + (rng.random(A.shape) < 0.004).astype(np.uint16), _rand_imgs(rng, 600, hi=4, density=0.05)])
+    D = oracle_mod.crss_matrix(A, H)
+    thr = D[np.arange(700), rng.integers(0, H.shape[0], 700)].copy()
+    got = rici.rici_crss_count_below(_dev(A), _dev(H), torch.from_numpy(thr.view(np.int64)).to(DEV))
+    assert np.array_equal(got.cpu().numpy().astype(np.int64), (D < thr[:, None]).sum(1))
+    r = rici.rici_crss_search(_dev(A), _dev(H)).cpu().numpy()
+    assert np.array_equal(r.astype(np.uint32), oracle_mod.ranks(A, H))
