@@ -1,5 +1,6 @@
-"""C4 rank mode on the tensor path: time per choice of prune-check prefixes
-(RICI_RANK_PREFIXES bit mask: 1 = rows 28-35, 2 = rows 24-39, 4 = rows 16-47)."""
+"""C4 rank mode on the tensor path: time per choice of prune-check prefixes (bit mask: 1 = rows
+28-35, 2 = rows 24-39, 4 = rows 16-47) in RICI_RANK_PREFIXES (dense passes) or, with
+PREFIX_VAR=RICI_RANK_PREFIXES_SP, in the 2:4-sparse passes (bits 2 and 4 only)."""
 import json, os, subprocess, sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -20,7 +21,8 @@ for _ in range(3):
     torch.cuda.synchronize(); ts.append((time.perf_counter() - t) * 1e3)
 print(json.dumps({"ms": float(np.median(ts)), "same": bool(torch.equal(r, full))}))
 ''' % ROOT
+var = os.environ.get("PREFIX_VAR", "RICI_RANK_PREFIXES")
 for mask in [int(x) for x in (sys.argv[1:] or ["6", "7", "2", "3", "4", "5", "1"])]:
-    env = dict(os.environ, RICI_RANK_PREFIXES=str(mask))
+    env = dict(os.environ, **{var: str(mask)})
     r = subprocess.run([sys.executable, "-c", CODE], env=env, capture_output=True, text=True)
     print(json.dumps({"mask": mask, "res": r.stdout.strip(), "err": r.stderr.strip()[-300:]}), flush=True)
