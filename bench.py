@@ -242,7 +242,7 @@ def run_gpu(args):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > L2 (126 MB)
     stream = torch.cuda.current_stream()
 
-    ev = {k: [] for k in ("step", "gen", "crss")}
+    ev = {k: [] for k in ("step", "mesh", "gen", "crss")}
 
     def step(record: bool):
         e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
@@ -262,6 +262,7 @@ def run_gpu(args):
         mesh.destroy()
         if record:
             ev["step"].append((e[0], e[3]))
+            ev["mesh"].append((e[0], e[1]))
             ev["gen"].append((e[1], e[2]))
             ev["crss"].append((e[2], e[3]))
 
@@ -295,7 +296,7 @@ def run_gpu(args):
     def ms(k):
         return float(np.mean([a.elapsed_time(b) for a, b in ev[k]]))
 
-    step_ms, gen_ms, crss_ms = ms("step"), ms("gen"), ms("crss")
+    step_ms, gen_ms, crss_ms, mesh_ms = ms("step"), ms("gen"), ms("crss"), ms("mesh")
     step_ms_max = step_ms
     if world > 1:
         t = torch.tensor([step_ms, gen_ms, crss_ms, gen_kernel_ms, mma_kernel_ms], dtype=torch.float64, device=dev)
@@ -474,6 +475,7 @@ def run_gpu(args):
             "comparisons_per_s": comparisons * world / (step_ms_max / 1e3),
             "construction": construction,
             "crss": {"ms": crss_ms, "comparisons_per_s": comparisons / crss_s},
+            "mesh_staging_ms": mesh_ms,
             "crss_simt_path": simt_line,
             "roofline": roof, "cpu_baseline": cb, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk.summary(), "bench_wall_s": wall}
