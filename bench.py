@@ -367,7 +367,8 @@ def run_gpu(args):
         K = 2 * 4096
         kern_s = mma_kernel_ms / 1e3                               # the GEMM launches, live events
         achieved = comparisons * 2.0 * K / kern_s / 1e12          # logical int8 ops/s (Tops/s)
-        derived = 2.0 * pk.get("bf16_tflops", 1587.6)              # measured bf16 x nominal ratio
+        # measured bf16 x the guide's nominal ratio for this dtype (dense int8 2x, 2:4 int8 4x)
+        derived = (4.0 if sparse else 2.0) * pk.get("bf16_tflops", 1587.6)
         arch = SMS * 8192 * 2 * sm_mhz * 1e6 / 1e12                # 8192 int8 MAC/clk/SM at sm_max
         sp_rate = None
         try:
@@ -396,9 +397,9 @@ def run_gpu(args):
                                 "doubled vendor figures are the 2:4 ones); the measured sparse issue rate is "
                                 "profiles/int8_sparse_rate.json" if sparse else
                                 "nominal dense int8 4.5 POPS (B200_PROFILING.md table)") +
-                               f".  The measured-derived dense figure (bf16 dense burst {pk.get('bf16_tflops', 1587.6)}"
-                               f" x 2 = {derived:.0f}) and cuBLAS int8 (profiles/int8_peak.json) are power-limited on "
-                               "random operands",
+                               f".  The measured-derived figure (bf16 dense burst {pk.get('bf16_tflops', 1587.6)}"
+                               f" x {4 if sparse else 2} = {derived:.0f}) and cuBLAS int8 (profiles/int8_peak.json) "
+                               "are power-limited on random operands",
                 "frac_vs_measured_sparse_rate": (achieved / sp_rate) if (sparse and sp_rate) else None,
                 "dense_equivalent_frac_of_dense_peak": achieved / 4500.0,
                 "frac_vs_measured_derived": achieved / derived,
