@@ -560,3 +560,17 @@ def test_sparse_needle_path_mixed(rici, oracle_mod):
     assert np.array_equal(got.cpu().numpy().astype(np.int64), (D < thr[:, None]).sum(1))
     r = rici.rici_crss_search(_dev(A), _dev(H)).cpu().numpy()
     assert np.array_equal(r.astype(np.uint32), oracle_mod.ranks(A, H))
+
+
+@pytest.mark.parametrize("nn,nh", [(900, 200), (513, 225), (260, 1)])
+def test_count_below_odd_shapes_sparse_path(rici, oracle_mod, nn, nh):
+    """count_below through the default (2:4-sparse) tensor path with shapes that stress the
+    tilings: more needles than haystack images, a haystack one past a 224 tile, a single
+    haystack image; exact against the oracle."""
+    rng = np.random.default_rng(nn + nh)
+    A = _rand_imgs(rng, nn, hi=4, density=0.03)
+    H = _rand_imgs(rng, nh, hi=4, density=0.03)
+    D = oracle_mod.crss_matrix(A, H)
+    thr = D[np.arange(nn), rng.integers(0, nh, nn)].copy() + rng.integers(0, 3, nn).astype(np.uint64)
+    got = rici.rici_crss_count_below(_dev(A), _dev(H), torch.from_numpy(thr.view(np.int64)).to(DEV))
+    assert np.array_equal(got.cpu().numpy().astype(np.int64), (D < thr[:, None]).sum(1))
