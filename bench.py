@@ -256,7 +256,7 @@ def run_gpu(args):
         else:
             if rank == 0:
                 needles.copy_(imgs)
-            dist.broadcast(needles, 0)
+            rdist.broadcast_images(needles, 0)
             rdist.search_sharded(needles, imgs, rank * n, N)
         e[3].record(stream)
         mesh.destroy()
@@ -318,7 +318,7 @@ def run_gpu(args):
         else:
             if rank == 0:
                 needles.copy_(imgs)
-            dist.broadcast(needles, 0)
+            rdist.broadcast_images(needles, 0)
             rh.copy_(rdist.search_sharded(needles, imgs, rank * n, N).to(torch.int32))   # D2H
         mesh.destroy()
     for _ in range(2):

@@ -54,6 +54,27 @@ def generate_sharded(mesh, origins: torch.Tensor, support_radius: float, n_bins:
     return generate(mesh, origins[lo:hi].contiguous(), support_radius, n_bins), (lo, hi)
 
 
+def broadcast_images(images: torch.Tensor, src: int = 0, group=None) -> torch.Tensor:
+    """Broadcast ``images`` (uint16 counts in int16 storage, in place) from ``src``.  When every
+    count fits a byte -- RICI counts of one object rarely exceed a few tens -- the payload goes
+    as uint8, half the bytes; otherwise the raw bytes (neither NCCL nor gloo has an int16
+    type).  Exact either way."""
+    dev = images.device
+    small = torch.zeros(1, dtype=torch.int32, device=dev)
+    if dist.get_rank(group) == src and images.numel():
+        small.fill_(int(images.view(torch.int16).to(torch.int32).bitwise_and(0xFFFF).max().item() <= 255))
+    dist.broadcast(small, src, group=group)
+    if not int(small.item()):
+        dist.broadcast(images.view(torch.uint8), src, group=group)   # NCCL/gloo have no int16: bytes
+        return images
+    packed = images.to(torch.uint8) if dist.get_rank(group) == src else torch.empty(images.shape, dtype=torch.uint8,
+                                                                                     device=dev)
+    dist.broadcast(packed, src, group=group)
+    if dist.get_rank(group) != src:
+        images.copy_(packed.to(torch.int16))
+    return images
+
+
 def search_sharded(needles: torch.Tensor, haystack_shard: torch.Tensor, shard_lo: int,
                    n_bins: int = 64, group=None, ops: SearchOps | None = None) -> torch.Tensor:
     """Ranks of needle i's correspondence haystack i over the union of all ranks' shards.

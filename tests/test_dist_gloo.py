@@ -13,7 +13,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2007_02306_b200.dist import SearchOps, generate_sharded, search_sharded, shard_range
+from paper_2007_02306_b200.dist import SearchOps, broadcast_images, generate_sharded, search_sharded, shard_range
 
 
 def test_shard_range_partitions():
@@ -70,8 +70,16 @@ def _worker(rank, world, port, needles, haystack, origins, q):
         nh = haystack.shape[0]
         slo, shi = shard_range(nh, world, rank)
         shard = torch.from_numpy(haystack[slo:shi].view(np.int16))
-        ranks = search_sharded(torch.from_numpy(needles.view(np.int16)), shard, slo, 64, ops=_oracle_ops())
-        q.put((rank, ranks.numpy(), gathered if rank == 0 else None))
+        # needles from rank 0 only (the bench's layout): small counts go as uint8, large as is
+        nd = torch.from_numpy(needles.view(np.int16).copy()) if rank == 0 else torch.zeros(needles.shape, dtype=torch.int16)
+        broadcast_images(nd, 0)
+        big = torch.from_numpy(needles.view(np.int16).copy()) if rank == 0 else torch.zeros(needles.shape, dtype=torch.int16)
+        if rank == 0:
+            big[0, 0, 5] = -2                                        # 65534 as uint16: full width
+        broadcast_images(big, 0)
+        bcast_ok = bool(torch.equal(nd, torch.from_numpy(needles.view(np.int16)))) and int(big[0, 0, 5]) == -2
+        ranks = search_sharded(nd, shard, slo, 64, ops=_oracle_ops())
+        q.put((rank, ranks.numpy(), gathered if rank == 0 else None, bcast_ok))
     finally:
         dist.destroy_process_group()
 
@@ -97,7 +105,8 @@ def test_sharded_search_and_generate_equal_single_process(oracle_mod, world):
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    for rank, ranks, gathered in res:
+    for rank, ranks, gathered, bcast_ok in res:
+        assert bcast_ok, rank
         assert np.array_equal(ranks.astype(np.uint32), want), rank
         if gathered is not None:
             parts = sorted(gathered, key=lambda g: g[0])
