@@ -301,8 +301,9 @@ def test_rank_mode_tensor_pruning_exact(rici, oracle_mod, seed):
 
 def test_crss_paths_agree_subprocess(tmp_path):
     """The SIMT path (RICI_CRSS_PATH=simt) and the four tensor-core kernels (RICI_MMA_MODE 0:
-    1-CTA, 1: 2-CTA multicast, 2: cta_group::2, 3: cta_group::2 with 2:4-sparse needle rows)
-    give identical ranks and counts."""
+    1-CTA, 1: 2-CTA multicast, 2: cta_group::2, 3: cta_group::2 with 2:4-sparse needle rows, one
+    or two haystack tiles per staged needle block, RICI_SP_NT, with and without a haystack slice
+    on the SMs the 4-CTA clusters leave free, RICI_SP_SIDE_FRAC) give identical ranks and counts."""
     import os
     import subprocess
     import sys
@@ -319,12 +320,15 @@ def test_crss_paths_agree_subprocess(tmp_path):
         "cnt = r.rici_crss_count_below(im[:2000], im, thr).cpu().numpy()\n"
         "np.save(sys.argv[1], np.concatenate([ranks.astype(np.int64), cnt.astype(np.int64)]))\n") % root
     outs = {}
-    for path, mode in (("simt", "2"), ("mma", "0"), ("mma", "1"), ("mma", "2"), ("mma", "3")):
-        env = dict(os.environ, RICI_CRSS_PATH=path, RICI_MMA_MODE=mode)
-        f = str(tmp_path / f"{path}{mode}.npy")
+    for path, mode, nt, side in (("simt", "2", "2", "0"), ("mma", "0", "2", "0"), ("mma", "1", "2", "0"),
+                                 ("mma", "2", "2", "0"), ("mma", "3", "1", "0"), ("mma", "3", "2", "0"),
+                                 ("mma", "3", "1", "0.3"), ("mma", "3", "2", "0.3")):
+        env = dict(os.environ, RICI_CRSS_PATH=path, RICI_MMA_MODE=mode, RICI_SP_NT=nt, RICI_SP_SIDE_FRAC=side)
+        key = f"{path}{mode}_{nt}_{side}"
+        f = str(tmp_path / f"{key}.npy")
         subprocess.run([sys.executable, "-c", code, f], env=env, check=True, timeout=600)
-        outs[path + mode] = np.load(f)
-    ref = outs.pop("simt2")
+        outs[key] = np.load(f)
+    ref = outs.pop("simt2_2_0")
     assert ref[2000:].max() > 0                              # the counts are not trivially zero
     for k, v in outs.items():
         assert np.array_equal(ref, v), k
@@ -562,10 +566,10 @@ def test_sparse_needle_path_mixed(rici, oracle_mod):
     assert np.array_equal(r.astype(np.uint32), oracle_mod.ranks(A, H))
 
 
-@pytest.mark.parametrize("nn,nh", [(900, 200), (513, 225), (260, 1)])
+@pytest.mark.parametrize("nn,nh", [(900, 200), (513, 225), (513, 449), (1100, 671), (260, 1)])
 def test_count_below_odd_shapes_sparse_path(rici, oracle_mod, nn, nh):
     """count_below through the default (2:4-sparse) tensor path with shapes that stress the
-    tilings: more needles than haystack images, a haystack one past a 224 tile, a single
+    tilings: more needles than haystack images, a haystack one past a 224 (and a 448) tile, a single
     haystack image; exact against the oracle."""
     rng = np.random.default_rng(nn + nh)
     A = _rand_imgs(rng, nn, hi=4, density=0.03)
