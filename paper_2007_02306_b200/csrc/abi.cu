@@ -302,9 +302,13 @@ rici_status rici_create_mesh(const float *vertices, int64_t n_vertices, const in
             (e = st.in(indices, sizeof(int32_t) * 3 * (size_t)n_triangles, &di)) == cudaSuccess &&
             (e = cudaMallocAsync((void **)&d_bad, sizeof(int), s)) == cudaSuccess) {
             st.temps.push_back(d_bad);
+            // the index check is synchronous, but waits only for the validating first pass: the
+            // sort and staging kernels are enqueued after it and run while the caller continues
+            float *centroid = nullptr;
             if ((e = cudaMemsetAsync(d_bad, 0, sizeof(int), s)) == cudaSuccess)
-                e = rici::launch_mesh_stage((const float *)dv, n_vertices, (const int32_t *)di,
-                                            n_triangles, &mesh->m, d_bad, s);
+                e = rici::launch_mesh_stage_begin((const float *)dv, n_vertices, (const int32_t *)di,
+                                                  n_triangles, &mesh->m, d_bad, &centroid, s);
+            if (centroid) st.temps.push_back(centroid);           // freed stream-ordered on any exit
             int bad = 0;
             if (e == cudaSuccess) e = cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, s);
             if (e == cudaSuccess) e = cudaStreamSynchronize(s);
@@ -313,6 +317,9 @@ rici_status rici_create_mesh(const float *vertices, int64_t n_vertices, const in
                 return fail(RICI_ERR_INVALID_ARGUMENT, "triangle index out of range [0, %lld)",
                             (long long)n_vertices);
             }
+            if (e == cudaSuccess)
+                e = rici::launch_mesh_stage_end((const float *)dv, n_vertices, (const int32_t *)di,
+                                                n_triangles, &mesh->m, centroid, s);
         }
         if (e != cudaSuccess) { rici_destroy_mesh(mesh); return cuda_fail(e, "rici_create_mesh"); }
     } else {

@@ -109,20 +109,33 @@ super_sphere_kernel(const float4 *__restrict__ sphere, int64_t n_chunks, float4 
 
 }  // namespace
 
-cudaError_t launch_mesh_stage(const float *d_vertices, int64_t nv, const int32_t *d_indices,
-                              int64_t nt, DeviceMesh *m, int *d_bad, cudaStream_t s) {
+// Two phases so the caller's synchronous index check waits only for the validating centroid
+// pass: begin() launches it (and allocates the sort keys), end() enqueues the spatial sort and
+// the staging kernels after the check has passed, and returns without waiting.  The caller
+// owns (and frees) the sort-key buffer begin() allocates.
+cudaError_t launch_mesh_stage_begin(const float *d_vertices, int64_t nv, const int32_t *d_indices,
+                                    int64_t nt, DeviceMesh *m, int *d_bad, float **centroid_out, cudaStream_t s) {
     m->nt = nt;
     m->n_chunks = (nt + kChunk - 1) / kChunk;
     m->n_super = (m->n_chunks + kSuper - 1) / kSuper;
+    *centroid_out = nullptr;
     if (m->n_chunks == 0) return cudaSuccess;
     cudaError_t e;
     float *centroid = nullptr;
     if ((e = cudaMallocAsync((void **)&centroid, sizeof(float) * 3 * nt, s)) != cudaSuccess) return e;
+    *centroid_out = centroid;
     if ((e = cudaMallocAsync((void **)&m->order, sizeof(int) * nt, s)) != cudaSuccess) return e;
-    int *order = m->order;
     int blocks = (int)std::min<int64_t>((nt + 255) / 256, 148 * 8);
     centroid_kernel<<<blocks, 256, 0, s>>>(d_vertices, nv, d_indices, nt, centroid, d_bad);
     note_launches(1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_mesh_stage_end(const float *d_vertices, int64_t nv, const int32_t *d_indices,
+                                  int64_t nt, DeviceMesh *m, float *centroid, cudaStream_t s) {
+    if (m->n_chunks == 0) return cudaSuccess;
+    cudaError_t e;
+    int *order = m->order;
     if ((e = spatial_order(centroid, 3, nt, order, s)) != cudaSuccess) return e;
     const int warps = 8;
     int64_t b2 = (m->n_chunks + warps - 1) / warps;
@@ -131,9 +144,7 @@ cudaError_t launch_mesh_stage(const float *d_vertices, int64_t nv, const int32_t
     int64_t b3 = (m->n_super + warps - 1) / warps;
     super_sphere_kernel<<<(unsigned)b3, 32 * warps, 0, s>>>(m->sphere, m->n_chunks, m->super_sphere, m->n_super);
     note_launches(2);
-    e = cudaGetLastError();
-    cudaFreeAsync(centroid, s);
-    return e;
+    return cudaGetLastError();                    // the caller frees centroid (stream-ordered)
 }
 
 }  // namespace rici

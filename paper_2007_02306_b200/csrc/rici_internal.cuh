@@ -42,8 +42,10 @@ cudaError_t ensure_smem(const void *kernel, size_t bytes);
 constexpr int64_t kMaxTriangles = ((int64_t)1 << 23) * 32;
 
 // a1: de-index + chunk layout + chunk spheres; *d_bad set to 1 on an out-of-range index.
-cudaError_t launch_mesh_stage(const float *d_vertices, int64_t nv, const int32_t *d_indices,
-                              int64_t nt, DeviceMesh *m, int *d_bad, cudaStream_t s);
+cudaError_t launch_mesh_stage_begin(const float *d_vertices, int64_t nv, const int32_t *d_indices,
+                                    int64_t nt, DeviceMesh *m, int *d_bad, float **centroid_out, cudaStream_t s);
+cudaError_t launch_mesh_stage_end(const float *d_vertices, int64_t nv, const int32_t *d_indices,
+                                  int64_t nt, DeviceMesh *m, float *centroid, cudaStream_t s);
 
 // a2-a8: RICI construction.
 cudaError_t launch_generate(const DeviceMesh &m, const float *d_origins, int64_t n, float R,
