@@ -171,6 +171,29 @@ __device__ __forceinline__ void project_z(const Frame &f, const float *v, float 
     }
 }
 
+// Eqs. 3-4 for T_x, T_y of the three translated vertices p (project_z output).
+__device__ __forceinline__ void project_xy(const Frame &f, const float *p, float *x, float *y) {
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        float qx = fmaf(f.nax, p[3 * j], f.nay * p[3 * j + 1]);
+        y[j] = fmaf(-f.nay, p[3 * j], f.nax * p[3 * j + 1]);
+        x[j] = fmaf(f.nbz, qx, -f.nbx * p[3 * j + 2]);
+    }
+}
+// alpha cull: if the triangle's (T_x, T_y) bounding box misses the disk of radius R, every
+// slice point has alpha > R > rho_{N-1} and no bin can be hit (exact skip)
+__device__ __forceinline__ bool alpha_box_hits(const float *x, const float *y, float r2) {
+    const float bx0 = fmaxf(fmaxf(fminf(x[0], fminf(x[1], x[2])), -fmaxf(x[0], fmaxf(x[1], x[2]))), 0.f);
+    const float by0 = fmaxf(fmaxf(fminf(y[0], fminf(y[1], y[2])), -fmaxf(y[0], fmaxf(y[1], y[2]))), 0.f);
+    return bx0 * bx0 + by0 * by0 <= r2;
+}
+
+// RICI_GEN_ALPHA_EARLY: the alpha-box test runs in the queue phase (with the beta-extent test),
+// so only pairs with rasterisation work are queued and every drained lane has a triangle
+#ifndef RICI_GEN_ALPHA_EARLY
+#define RICI_GEN_ALPHA_EARLY 1
+#endif
+
 // K <= 2 (N = 64 default): 32 KB of counters, so smem admits 5 CTAs / SM; cap the registers
 // (48, a few bytes of spill) so the register file admits them too -- measured 3.34 -> 3.09 ms on C2
 template <int K>
@@ -258,17 +281,8 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
             float p[9], z[3];
             project_z(f, v, p, z);
             float x[3], y[3];
-#pragma unroll
-            for (int j = 0; j < 3; ++j) {                // Eqs. 3-4 for T_x, T_y
-                float qx = fmaf(f.nax, p[3 * j], f.nay * p[3 * j + 1]);
-                y[j] = fmaf(-f.nay, p[3 * j], f.nax * p[3 * j + 1]);
-                x[j] = fmaf(f.nbz, qx, -f.nbx * p[3 * j + 2]);
-            }
-            // alpha cull: if the triangle's (T_x, T_y) bounding box misses the disk of radius R,
-            // every slice point has alpha > R > rho_{N-1} and no bin can be hit (exact skip)
-            const float bx0 = fmaxf(fmaxf(fminf(x[0], fminf(x[1], x[2])), -fmaxf(x[0], fmaxf(x[1], x[2]))), 0.f);
-            const float by0 = fmaxf(fmaxf(fminf(y[0], fminf(y[1], y[2])), -fmaxf(y[0], fmaxf(y[1], y[2]))), 0.f);
-            if (bx0 * bx0 + by0 * by0 <= g.r2) {
+            project_xy(f, p, x, y);                      // Eqs. 3-4 for T_x, T_y
+            if (RICI_GEN_ALPHA_EARLY || alpha_box_hits(x, y, g.r2)) {
                 RICI_STAT(3, 1);
                 float ax = x[0], ay = y[0], az = z[0], bx = x[1], by = y[1], bz = z[1],
                       cx = x[2], cy = y[2], cz = z[2];
@@ -380,6 +394,13 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
                             float zlo = fminf(z[0], fminf(z[1], z[2])), zhi = fmaxf(z[0], fmaxf(z[1], z[2]));
                             keep[k] = first_at_or_above(zlo, g.inv_delta, g.row_off, N) <
                                       first_at_or_above(zhi, g.inv_delta, g.row_off, N);
+#if RICI_GEN_ALPHA_EARLY
+                            if (keep[k]) {
+                                float x[3], y[3];
+                                project_xy(f, p, x, y);
+                                keep[k] = alpha_box_hits(x, y, g.r2);
+                            }
+#endif
                         }
                     }
 #pragma unroll
