@@ -219,7 +219,12 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
     const int64_t img0 = (int64_t)blockIdx.x * K;
     const int k_valid = (int)min((int64_t)K, n - img0);
 
-    for (int i = tid; i < K * img_words; i += kThreads) acc[i] = 0;
+    {
+        const int nw = K * img_words;
+        int4 *a4 = reinterpret_cast<int4 *>(acc);              // dynamic smem: 16-byte aligned
+        for (int i = tid; i < nw / 4; i += kThreads) a4[i] = make_int4(0, 0, 0, 0);
+        for (int i = (nw / 4) * 4 + tid; i < nw; i += kThreads) acc[i] = 0;
+    }
     if (tid < K) {
         if (tid < k_valid) {
             const int idx = img_perm ? img_perm[img0 + tid] : (int)(img0 + tid);
@@ -269,6 +274,8 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
         __syncwarp();
         if (lane < rest) queue[warp][lane] = moved;
         qn = rest;
+        int stat_rows = 0;                               // RICI_GEN_STATS: layer-loop length
+        (void)stat_rows;
         if (item >= 0) {
             RICI_STAT(2, 1);
             const int64_t chunk = (int64_t)((unsigned)item >> 8);
@@ -287,9 +294,19 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
                 float ax = x[0], ay = y[0], az = z[0], bx = x[1], by = y[1], bz = z[1],
                       cx = x[2], cy = y[2], cz = z[2];
                 sort3(ax, ay, az, bx, by, bz, cx, cy, cz);
+#if RICI_GEN_STATS
+                stat_rows = max(0, first_at_or_above(cz, g.inv_delta, g.row_off, g.n) -
+                                       first_at_or_above(az, g.inv_delta, g.row_off, g.n));
+#endif
                 rasterise_triangle(acc_s + 4u * (unsigned)(k * img_words), g, ax, ay, az, bx, by, bz, cx, cy, cz);
             }
         }
+#if RICI_GEN_STATS
+        {   // warp iterations of the layer loop (the longest lane) and drains
+            const int mx = __reduce_max_sync(0xffffffffu, stat_rows);
+            if (lane == 0) { RICI_STAT(6, mx); RICI_STAT(7, 1); }
+        }
+#endif
         __syncwarp();
     };
 
@@ -421,9 +438,33 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
     }
     __syncthreads();
 
-    // Epilogue: per-row inclusive prefix sum of the difference arrays (warp per row), then
-    // saturate to uint16 (G9) and store the row at its image's caller index -- lane l holds
-    // columns [l*cpl, l*cpl + cpl), written as packed pairs when aligned.
+    // Epilogue: per-row inclusive prefix sum of the difference arrays, saturated to uint16 (G9),
+    // stored at the image's caller index.  N = 64 (16-byte aligned output): one thread per row,
+    // a sequential running sum over the 64 columns (row r of a [64][65] array starts in bank
+    // r mod 32, so a warp's 32 rows read 32 distinct banks), eight 16-byte stores per row.
+    if (N == 64 && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+        for (int rr = tid; rr < k_valid * 64; rr += kThreads) {
+            const int k = rr >> 6, r = rr & 63;
+            const int *rp = acc + k * img_words + r * 65;
+            uint4 *dst = reinterpret_cast<uint4 *>(out + (int64_t)img_idx[k] * 4096 + r * 64);
+            unsigned run = 0;
+#pragma unroll
+            for (int c8 = 0; c8 < 8; ++c8) {
+                unsigned w[4];
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    run += (unsigned)rp[8 * c8 + 2 * h];
+                    const unsigned lo = min(run, 65535u);
+                    run += (unsigned)rp[8 * c8 + 2 * h + 1];
+                    w[h] = lo | (min(run, 65535u) << 16);
+                }
+                dst[c8] = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+        }
+        return;
+    }
+    // any N: warp per row -- lane l holds columns [l*cpl, l*cpl + cpl), written as packed pairs
+    // when aligned.
     const int npix = N * N;
     const int cpl = (N + 31) / 32;                 // columns per lane
     const bool pairs = (cpl % 2) == 0 && (N % 2) == 0 && (reinterpret_cast<uintptr_t>(out) & 3) == 0;

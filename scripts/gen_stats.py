@@ -22,7 +22,8 @@ buf = (ctypes.c_ulonglong * 8)()
 rici.rici_generate(mesh, o, 0.3, 64); lib.rici_debug_gen_stats(buf, 1)
 rici.rici_generate(mesh, o, 0.3, 64); lib.rici_debug_gen_stats(buf, 1)
 n = m.n_vertices
-names = ["chunk_visits", "chunk_image_pairs", "queued_pairs", "alpha_pass_pairs", "rows", "segments"]
+names = ["chunk_visits", "chunk_image_pairs", "queued_pairs", "alpha_pass_pairs", "rows", "segments",
+         "layer_loop_warp_iterations", "drains"]
 res = {k: buf[i] / n for i, k in enumerate(names)}
 res["triangle_pairs_tested"] = res["chunk_image_pairs"] * 32
 print(json.dumps({"per_image": res, "images": n}))
