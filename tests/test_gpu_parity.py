@@ -303,7 +303,8 @@ def test_crss_paths_agree_subprocess(tmp_path):
     """The SIMT path (RICI_CRSS_PATH=simt) and the four tensor-core kernels (RICI_MMA_MODE 0:
     1-CTA, 1: 2-CTA multicast, 2: cta_group::2, 3: cta_group::2 with 2:4-sparse needle rows, one
     or two haystack tiles per staged needle block, RICI_SP_NT, with and without a haystack slice
-    on the SMs the 4-CTA clusters leave free, RICI_SP_SIDE_FRAC) give identical ranks and counts."""
+    on the SMs the 4-CTA clusters leave free, RICI_SP_SIDE_FRAC) give identical ranks and counts, in
+    full mode and in rank mode (early exit: tile pruning on K prefixes)."""
     import os
     import subprocess
     import sys
@@ -314,11 +315,14 @@ def test_crss_paths_agree_subprocess(tmp_path):
         "m = synth.bumpy_torus(120, 60, key=(31,))\n"
         "mesh = r.rici_create_mesh(torch.from_numpy(m.vertices).cuda(), torch.from_numpy(m.indices).cuda())\n"
         "im = r.rici_generate(mesh, torch.from_numpy(m.origins).cuda(), 0.3, 64)\n"
-        "ranks = r.rici_crss_search(im[:2000], im).cpu().numpy()\n"
+        "nee = im[:2000].clone(); nee[:, ::7, 5::9] += 1   # perturbed needles: thresholds > 0\n"
+        "nee[1::2] = im[(torch.arange(1, 2000, 2, device='cuda') * 7 + 3) %% im.shape[0]]   # wrong matches: large ranks\n"
+        "ranks = r.rici_crss_search(nee, im).cpu().numpy()\n"
         "pr = torch.stack([torch.arange(2000), (torch.arange(2000) * 7919) %% im.shape[0]], 1).cuda()\n"
-        "thr = r.rici_crss_pairs(im[:2000], im, pr)\n"
-        "cnt = r.rici_crss_count_below(im[:2000], im, thr).cpu().numpy()\n"
-        "np.save(sys.argv[1], np.concatenate([ranks.astype(np.int64), cnt.astype(np.int64)]))\n") % root
+        "thr = r.rici_crss_pairs(nee, im, pr)\n"
+        "cnt = r.rici_crss_count_below(nee, im, thr).cpu().numpy()\n"
+        "early = r.rici_crss_search(nee, im, early_exit=True).cpu().numpy()\n"
+        "np.save(sys.argv[1], np.concatenate([ranks.astype(np.int64), cnt.astype(np.int64), early.astype(np.int64)]))\n") % root
     outs = {}
     for path, mode, nt, side in (("simt", "2", "2", "0"), ("mma", "0", "2", "0"), ("mma", "1", "2", "0"),
                                  ("mma", "2", "2", "0"), ("mma", "3", "1", "0"), ("mma", "3", "2", "0"),
@@ -329,7 +333,8 @@ def test_crss_paths_agree_subprocess(tmp_path):
         subprocess.run([sys.executable, "-c", code, f], env=env, check=True, timeout=600)
         outs[key] = np.load(f)
     ref = outs.pop("simt2_2_0")
-    assert ref[2000:].max() > 0                              # the counts are not trivially zero
+    assert ref[:2000].max() > 0 and ref[2000:4000].max() > 0  # ranks and counts not trivially zero
+    assert np.array_equal(ref[:2000], ref[4000:])            # rank mode (early exit) = full mode
     for k, v in outs.items():
         assert np.array_equal(ref, v), k
 
