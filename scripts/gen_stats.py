@@ -15,7 +15,10 @@ sys.path.insert(0, d); sys.path.insert(1, ROOT)
 import torch
 import synth, paper_2007_02306_b200 as rici
 lib = ctypes.CDLL(os.path.join(d, "paper_2007_02306_b200", "librici.so"))
-cfg = synth.config_c2(); m = cfg["mesh"]
+if os.environ.get("WORKLOAD") == "c3":            # the 10-object clutterbox scene
+    cfg = synth.config_c3(); m = cfg["mesh"]
+else:
+    cfg = synth.config_c2(); m = cfg["mesh"]
 mesh = rici.rici_create_mesh(torch.from_numpy(m.vertices).cuda(), torch.from_numpy(m.indices).cuda())
 o = torch.from_numpy(cfg["origins"]).cuda()
 buf = (ctypes.c_ulonglong * 8)()
