@@ -39,7 +39,7 @@ namespace rici {
 namespace {
 
 #if RICI_GEN_STATS   // tuning builds only: event counters read by rici_debug_gen_stats
-__device__ unsigned long long g_stats[8];
+__device__ unsigned long long g_stats[10];
 #define RICI_STAT(i, v) atomicAdd(&g_stats[i], (unsigned long long)(v))
 #else
 #define RICI_STAT(i, v)
@@ -105,7 +105,10 @@ __device__ __forceinline__ void rasterise_triangle(unsigned acc, const Geometry 
     const int N = g.n;
     int r_lo = first_at_or_above(az, g.inv_delta, g.row_off, N);
     int r_hi = first_at_or_above(cz, g.inv_delta, g.row_off, N);
-    if (r_lo >= r_hi) return;
+    if (r_lo >= r_hi) { RICI_STAT(8, 1); return; }
+#if RICI_GEN_STATS
+    bool stat_emitted = false;
+#endif
     RICI_STAT(4, r_hi - r_lo);
     const float inv_ac = fast_rcp(cz - az);              // > 0 whenever a layer is inside
     const float inv_ab = bz > az ? fast_rcp(bz - az) : 0.f;
@@ -149,10 +152,16 @@ __device__ __forceinline__ void rasterise_triangle(unsigned acc, const Geometry 
         }
         if (c_lo == c_max) continue;                      // nothing in [c_lo, c_max)
         RICI_STAT(5, 1);
+#if RICI_GEN_STATS
+        stat_emitted = true;
+#endif
         red_shared(row + 4u * (unsigned)c_lo, dbl ? 2 : 1);
         if (dbl) red_shared(row + 4u * (unsigned)c_min, -1);
         red_shared(row + 4u * (unsigned)c_max, -1);
     }
+#if RICI_GEN_STATS
+    if (!stat_emitted) RICI_STAT(9, 1);            // rasterised pairs that emitted no segment
+#endif
 }
 
 // Work item of the survivor queue: (chunk, triangle lane, image) packed in 32 bits.
@@ -562,8 +571,8 @@ cudaError_t launch_generate(const DeviceMesh &m, const float *d_origins, int64_t
 #if RICI_GEN_STATS
 extern "C" __attribute__((visibility("default"))) int rici_debug_gen_stats(unsigned long long *out, int reset) {
     cudaDeviceSynchronize();
-    cudaMemcpyFromSymbol(out, rici::g_stats, sizeof(unsigned long long) * 8);
-    if (reset) { unsigned long long z[8] = {}; cudaMemcpyToSymbol(rici::g_stats, z, sizeof(z)); }
+    cudaMemcpyFromSymbol(out, rici::g_stats, sizeof(unsigned long long) * 10);
+    if (reset) { unsigned long long z[10] = {}; cudaMemcpyToSymbol(rici::g_stats, z, sizeof(z)); }
     return 0;
 }
 #endif
