@@ -206,7 +206,10 @@ __device__ __forceinline__ bool alpha_box_hits(const float *x, const float *y, f
 // K <= 2 (N = 64 default): 32 KB of counters, so smem admits 5 CTAs / SM; cap the registers
 // (48, a few bytes of spill) so the register file admits them too -- measured 3.34 -> 3.09 ms on C2
 template <int K>
-__global__ void __launch_bounds__(kThreads, K <= 2 ? 5 : 1)
+#ifndef RICI_GEN_MIN_BLOCKS
+#define RICI_GEN_MIN_BLOCKS 5
+#endif
+__global__ void __launch_bounds__(kThreads, K <= 2 ? RICI_GEN_MIN_BLOCKS : 1)
 generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere, int64_t n_chunks,
                 const float4 *__restrict__ super_sphere, int64_t n_super,
                 const float *__restrict__ origins, const int *__restrict__ img_perm, int64_t n,
