@@ -6,8 +6,9 @@
 // (a CTA's group) spatially compact, which is what makes the exact bounding-sphere cull
 // in generate.cu effective for arbitrarily ordered inputs.
 //
-// Method: counting sort of points by an 18-bit Morton code (6 bits per axis over the
-// points' bounding box): histogram (atomics), three-pass exclusive scan, scatter.
+// Method: counting sort of points by an 18-bit cell key (6 bits per axis over the points'
+// bounding box; Hilbert order, or Morton with -DRICI_SORT_HILBERT=0): histogram (atomics),
+// three-pass exclusive scan, scatter.
 #include <algorithm>
 
 #include "rici_internal.cuh"
@@ -57,6 +58,41 @@ __device__ __forceinline__ unsigned spread3(unsigned x) {   // 6 bits -> every t
     return r;
 }
 
+// Hilbert index of a cell (Skilling's transpose algorithm, kCellBits bits per axis): unlike the
+// Morton (Z) order, consecutive cells along the curve are always face neighbours, so a run of
+// 32 surface triangles -- a chunk -- does not jump across the volume between occupied cells
+// (C2 model: 19% fewer (image, triangle) pairs tested behind the chunk cull).
+#ifndef RICI_SORT_HILBERT
+#define RICI_SORT_HILBERT 1
+#endif
+__device__ __forceinline__ unsigned hilbert3(unsigned x0, unsigned x1, unsigned x2) {
+    unsigned X[3] = {x0, x1, x2};
+    const unsigned M = 1u << (kCellBits - 1);
+    for (unsigned Q = M; Q > 1; Q >>= 1) {        // inverse undo excess work
+        const unsigned P = Q - 1;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            if (X[i] & Q) {
+                X[0] ^= P;
+            } else {
+                const unsigned t = (X[0] ^ X[i]) & P;
+                X[0] ^= t;
+                X[i] ^= t;
+            }
+        }
+    }
+    X[1] ^= X[0];                                  // Gray encode
+    X[2] ^= X[1];
+    unsigned t = 0;
+    for (unsigned Q = M; Q > 1; Q >>= 1)
+        if (X[2] & Q) t ^= Q - 1;
+    X[0] ^= t; X[1] ^= t; X[2] ^= t;
+    unsigned h = 0;                                // transpose -> index
+    for (int b = kCellBits - 1; b >= 0; --b)
+        h = (h << 3) | (((X[0] >> b) & 1u) << 2) | (((X[1] >> b) & 1u) << 1) | ((X[2] >> b) & 1u);
+    return h;
+}
+
 __device__ __forceinline__ unsigned cell_of(const float *p, const int *box) {
     unsigned c[3];
     for (int a = 0; a < 3; ++a) {
@@ -66,7 +102,11 @@ __device__ __forceinline__ unsigned cell_of(const float *p, const int *box) {
         int q = (int)(t * (float)(1 << kCellBits));
         c[a] = (unsigned)min(max(q, 0), (1 << kCellBits) - 1);
     }
+#if RICI_SORT_HILBERT
+    return hilbert3(c[0], c[1], c[2]);
+#else
     return spread3(c[0]) | (spread3(c[1]) << 1) | (spread3(c[2]) << 2);
+#endif
 }
 
 __global__ void __launch_bounds__(256)
@@ -129,7 +169,7 @@ scatter_kernel(const unsigned *__restrict__ cell, int64_t n, int *__restrict__ o
 
 }  // namespace
 
-// perm[k] = index of the k-th point in Morton-cell order.  pts: n points, `stride` floats apart.
+// perm[k] = index of the k-th point in cell order (Hilbert curve over 64^3 cells).  pts: n points, `stride` floats apart.
 // Workspace is stream-ordered.
 cudaError_t spatial_order(const float *d_pts, int stride, int64_t n, int *d_perm, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
