@@ -16,7 +16,7 @@
 //    segment costs <= 3 branch-free shared reductions (+2 at col(|C|), -1 at col(min), -1 at
 //    col(max)) instead of one per covered bin; a warp-shuffle prefix scan per row turns them
 //    into counts in the epilogue;
-//  * images are built in spatial (Morton-cell) order and the mesh is stored in spatially
+//  * images are built in spatial (Hilbert-cell) order and the mesh is stored in spatially
 //    compact chunks of 32 triangles (mesh.cu, sort.cu); an exact three-level cull skips
 //    triangles that cannot reach any of the CTA's support volumes: superchunk spheres and
 //    chunk spheres vs the CTA sphere, then chunk sphere vs each image's support CYLINDER;

@@ -3,7 +3,7 @@
 // "iterate over each triangle in the scene": the construction kernel streams every
 // triangle once per group of images, so the indexed mesh (vertices + index triples, D1) is
 // de-indexed once into a device buffer laid out for that stream:
-//  * triangles in spatial order (an 18-bit Morton cell of the centroid, counting sort in
+//  * triangles in spatial order (an 18-bit Hilbert cell key of the centroid, counting sort in
 //    sort.cu) -- an internal reordering that cannot change any image, counts being sums
 //    over triangles; the permutation is kept for per-triangle tags (rici_clutter_fraction);
 //  * chunks of 32 triangles, structure-of-arrays inside a chunk, so one warp reads a chunk

@@ -16,7 +16,7 @@ struct DeviceMesh {
     int64_t nt = 0;               // triangles
     int64_t n_chunks = 0;         // ceil(nt / kChunk)
     int64_t n_super = 0;          // ceil(n_chunks / kSuper)
-    float *tri = nullptr;         // [n_chunks][9][kChunk], triangles in spatial (Morton-cell) order
+    float *tri = nullptr;         // [n_chunks][9][kChunk], triangles in spatial (Hilbert-cell) order
     float4 *sphere = nullptr;     // [n_chunks] bounding sphere (cx, cy, cz, r) of each chunk
     float4 *super_sphere = nullptr;  // [n_super] bounding sphere of each superchunk
     int *order = nullptr;         // [nt] staged slot -> caller triangle index
