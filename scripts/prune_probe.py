@@ -20,7 +20,7 @@ nn, nh = ref.shape[0], sc.shape[0]
 tiles = [int(x) for x in np.linspace(0, nn // 256 - 1, 6)]
 def pairs(js):
     return [r for j in js for r in (2 * j, 2 * j + 1)]
-subsets = {"all": list(range(64)), "mid16": list(range(24, 40)), "mid32": list(range(16, 48)),
+subsets = {"all": list(range(64)), "mid16": list(range(24, 40)), "mid24": list(range(20, 44)), "mid32": list(range(16, 48)),
            "lo16": list(range(0, 16)),
            "spread16": pairs(range(1, 32, 4)), "spread16b": pairs(range(2, 32, 4)),
            "midspread16": pairs([8, 10, 12, 14, 17, 19, 21, 23]),

@@ -1,6 +1,6 @@
 """C4 rank mode on the tensor path: time per choice of prune-check prefixes (bit mask: 1 = rows
-28-35, 2 = rows 24-39, 4 = rows 16-47) in RICI_RANK_PREFIXES (dense passes) or, with
-PREFIX_VAR=RICI_RANK_PREFIXES_SP, in the 2:4-sparse passes (bits 2 and 4 only)."""
+28-35, 2 = rows 24-39, 4 = rows 16-47, 8 = rows 20-43) in RICI_RANK_PREFIXES (dense passes)
+or, with PREFIX_VAR=RICI_RANK_PREFIXES_SP, in the 2:4-sparse passes (bits 2, 4 and 8)."""
 import json, os, subprocess, sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
