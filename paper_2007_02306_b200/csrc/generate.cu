@@ -543,6 +543,10 @@ cudaError_t launch_generate(const DeviceMesh &m, const float *d_origins, int64_t
     cudaError_t e = cudaMallocAsync((void **)&perm, sizeof(int) * n, s);
     if (e != cudaSuccess) return e;
     if ((e = spatial_order(d_origins, 6, n, perm, s)) != cudaSuccess) return e;
+#ifndef RICI_GEN_KD_IMAGES
+#define RICI_GEN_KD_IMAGES 0
+#endif
+    if (RICI_GEN_KD_IMAGES && (e = kd_refine(d_origins, 6, n, perm, s)) != cudaSuccess) return e;
     int64_t blocks = (n + Kt - 1) / Kt;
     // the geometry lives in the kernel's parameter bank (no per-thread recomputation)
     Geometry g;

@@ -108,71 +108,6 @@ super_sphere_kernel(const float4 *__restrict__ sphere, int64_t n_chunks, float4 
     }
 }
 
-// Chunk partition inside each superchunk (kSuper * kChunk = 1024 triangles of the cell order):
-// a kd-tree of median splits down to 32-triangle leaves.  Cell order alone makes runs of 32
-// that straddle several cells; median splits along each node's longest centroid extent make
-// compact leaves, so the chunk spheres -- and the pairs the construction kernel tests behind
-// them -- shrink (C2 model: 22% fewer tested pairs).  The superchunks keep their triangle sets.
-// One CTA of 1024 threads per full superchunk, one triangle per thread: at each of the five
-// levels every node (a 1024 >> l aligned segment) is bitonic-sorted by its longest axis, and
-// its halves become the children.  The partial last superchunk keeps the cell order.
-constexpr int kKdBlock = kSuper * kChunk;
-__global__ void __launch_bounds__(kKdBlock)
-kd_chunks_kernel(const float *__restrict__ centroid, int *__restrict__ order, int64_t nt) {
-    static_assert(kKdBlock == 1024, "one thread per triangle of a superchunk");
-    __shared__ float xkey[2][kKdBlock];                    // double-buffered exchange (j >= 32)
-    __shared__ int xidx[2][kKdBlock];
-    __shared__ float wbox[kKdBlock / 32][6];
-    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    const int64_t base = (int64_t)blockIdx.x * kKdBlock;
-    if (base + kKdBlock > nt) return;                      // partial block: keep the cell order
-    int iv = order[base + t];
-    int buf = 0;
-    for (int S = kKdBlock; S > kChunk; S >>= 1) {
-        // this node's bounding box: warp reductions, then the warps of the node
-        const float c[3] = {centroid[3 * (int64_t)iv], centroid[3 * (int64_t)iv + 1], centroid[3 * (int64_t)iv + 2]};
-        float lo[3] = {c[0], c[1], c[2]}, hi[3] = {c[0], c[1], c[2]};
-#pragma unroll
-        for (int a = 0; a < 3; ++a)
-            for (int o = 16; o > 0; o >>= 1) {
-                lo[a] = fminf(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
-                hi[a] = fmaxf(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
-            }
-        if (lane == 0)
-            for (int a = 0; a < 3; ++a) { wbox[warp][a] = lo[a]; wbox[warp][3 + a] = hi[a]; }
-        __syncthreads();
-        const int w0 = (t / S) * (S / 32), nw = S / 32;
-        for (int w = w0; w < w0 + nw; ++w)
-            for (int a = 0; a < 3; ++a) { lo[a] = fminf(lo[a], wbox[w][a]); hi[a] = fmaxf(hi[a], wbox[w][3 + a]); }
-        const float ex = hi[0] - lo[0], ey = hi[1] - lo[1], ez = hi[2] - lo[2];
-        float kv = ex >= ey ? (ex >= ez ? c[0] : c[2]) : (ey >= ez ? c[1] : c[2]);
-        // bitonic sort of every aligned segment of S (ascending); partners within a warp by
-        // shuffle, farther ones through shared memory
-        for (int k = 2; k <= S; k <<= 1) {
-            const bool up = k == S || (t & k) == 0;
-            for (int j = k >> 1; j > 0; j >>= 1) {
-                float pk;
-                int pi;
-                if (j >= 32) {
-                    xkey[buf][t] = kv;
-                    xidx[buf][t] = iv;
-                    __syncthreads();
-                    pk = xkey[buf][t ^ j];
-                    pi = xidx[buf][t ^ j];
-                    buf ^= 1;
-                } else {
-                    pk = __shfl_xor_sync(0xffffffffu, kv, j);
-                    pi = __shfl_xor_sync(0xffffffffu, iv, j);
-                }
-                const bool lower = (t & j) == 0;           // keep the min iff lower == up
-                if (lower == up ? pk < kv : pk > kv) { kv = pk; iv = pi; }
-            }
-        }
-        __syncthreads();                                   // wbox reuse at the next level
-    }
-    order[base + t] = iv;
-}
-
 }  // namespace
 
 // Two phases so the caller's synchronous index check waits only for the validating centroid
@@ -206,10 +141,7 @@ cudaError_t launch_mesh_stage_end(const float *d_vertices, int64_t nv, const int
 #ifndef RICI_KD_CHUNKS
 #define RICI_KD_CHUNKS 1
 #endif
-    if (RICI_KD_CHUNKS && nt >= kKdBlock) {
-        kd_chunks_kernel<<<(unsigned)(nt / kKdBlock), kKdBlock, 0, s>>>(centroid, order, nt);
-        note_launches(1);
-    }
+    if (RICI_KD_CHUNKS && (e = kd_refine(centroid, 3, nt, order, s)) != cudaSuccess) return e;
     const int warps = 8;
     int64_t b2 = (m->n_chunks + warps - 1) / warps;
     mesh_stage_kernel<<<(unsigned)b2, 32 * warps, 0, s>>>(d_vertices, nv, d_indices, order, nt, m->tri,

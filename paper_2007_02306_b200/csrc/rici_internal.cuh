@@ -25,6 +25,8 @@ struct DeviceMesh {
 
 // perm[k] = index of the k-th of n points (stride floats apart) in spatial order.
 cudaError_t spatial_order(const float *d_pts, int stride, int64_t n, int *d_perm, cudaStream_t s);
+// kd-tree leaves of 32 inside every full block of 1024 of a spatial order (sort.cu)
+cudaError_t kd_refine(const float *d_pts, int stride, int64_t n, int *d_perm, cudaStream_t s);
 
 // Kernel-launch bookkeeping (rici_launch_count()).
 void note_launches(int k);

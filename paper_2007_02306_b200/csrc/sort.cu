@@ -52,19 +52,21 @@ bbox_kernel(const float *__restrict__ pts, int stride, int64_t n, int *__restric
     }
 }
 
+#ifndef RICI_SORT_HILBERT
+#define RICI_SORT_HILBERT 1
+#endif
+#if !RICI_SORT_HILBERT
 __device__ __forceinline__ unsigned spread3(unsigned x) {   // 6 bits -> every third bit
     unsigned r = 0;
     for (int b = 0; b < kCellBits; ++b) r |= ((x >> b) & 1u) << (3 * b);
     return r;
 }
+#endif
 
 // Hilbert index of a cell (Skilling's transpose algorithm, kCellBits bits per axis): unlike the
 // Morton (Z) order, consecutive cells along the curve are always face neighbours, so a run of
 // 32 surface triangles -- a chunk -- does not jump across the volume between occupied cells
 // (C2 model: 19% fewer (image, triangle) pairs tested behind the chunk cull).
-#ifndef RICI_SORT_HILBERT
-#define RICI_SORT_HILBERT 1
-#endif
 __device__ __forceinline__ unsigned hilbert3(unsigned x0, unsigned x1, unsigned x2) {
     unsigned X[3] = {x0, x1, x2};
     const unsigned M = 1u << (kCellBits - 1);
@@ -167,6 +169,72 @@ scatter_kernel(const unsigned *__restrict__ cell, int64_t n, int *__restrict__ o
         perm[atomicAdd(offs + cell[i], 1)] = (int)i;
 }
 
+// Chunk partition inside each superchunk (kSuper * kChunk = 1024 points of the cell order):
+// a kd-tree of median splits down to 32-triangle leaves.  Cell order alone makes runs of 32
+// that straddle several cells; median splits along each node's longest centroid extent make
+// compact leaves, so the chunk spheres -- and the pairs the construction kernel tests behind
+// them -- shrink (C2 model: 22% fewer tested pairs).  The superchunks keep their triangle sets.
+// One CTA of 1024 threads per full superchunk, one triangle per thread: at each of the five
+// levels every node (a 1024 >> l aligned segment) is bitonic-sorted by its longest axis, and
+// its halves become the children.  The partial last superchunk keeps the cell order.
+constexpr int kKdBlock = 1024;                 // = kSuper * kChunk
+__global__ void __launch_bounds__(kKdBlock)
+kd_chunks_kernel(const float *__restrict__ pts, int stride, int *__restrict__ order, int64_t nt) {
+    static_assert(kKdBlock == 1024, "one thread per triangle of a superchunk");
+    __shared__ float xkey[2][kKdBlock];                    // double-buffered exchange (j >= 32)
+    __shared__ int xidx[2][kKdBlock];
+    __shared__ float wbox[kKdBlock / 32][6];
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int64_t base = (int64_t)blockIdx.x * kKdBlock;
+    if (base + kKdBlock > nt) return;                      // partial block: keep the cell order
+    int iv = order[base + t];
+    int buf = 0;
+    for (int S = kKdBlock; S > kChunk; S >>= 1) {
+        // this node's bounding box: warp reductions, then the warps of the node
+        const float *pp = pts + (int64_t)stride * iv;
+        const float c[3] = {pp[0], pp[1], pp[2]};
+        float lo[3] = {c[0], c[1], c[2]}, hi[3] = {c[0], c[1], c[2]};
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+            for (int o = 16; o > 0; o >>= 1) {
+                lo[a] = fminf(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+                hi[a] = fmaxf(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+            }
+        if (lane == 0)
+            for (int a = 0; a < 3; ++a) { wbox[warp][a] = lo[a]; wbox[warp][3 + a] = hi[a]; }
+        __syncthreads();
+        const int w0 = (t / S) * (S / 32), nw = S / 32;
+        for (int w = w0; w < w0 + nw; ++w)
+            for (int a = 0; a < 3; ++a) { lo[a] = fminf(lo[a], wbox[w][a]); hi[a] = fmaxf(hi[a], wbox[w][3 + a]); }
+        const float ex = hi[0] - lo[0], ey = hi[1] - lo[1], ez = hi[2] - lo[2];
+        float kv = ex >= ey ? (ex >= ez ? c[0] : c[2]) : (ey >= ez ? c[1] : c[2]);
+        // bitonic sort of every aligned segment of S (ascending); partners within a warp by
+        // shuffle, farther ones through shared memory
+        for (int k = 2; k <= S; k <<= 1) {
+            const bool up = k == S || (t & k) == 0;
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                float pk;
+                int pi;
+                if (j >= 32) {
+                    xkey[buf][t] = kv;
+                    xidx[buf][t] = iv;
+                    __syncthreads();
+                    pk = xkey[buf][t ^ j];
+                    pi = xidx[buf][t ^ j];
+                    buf ^= 1;
+                } else {
+                    pk = __shfl_xor_sync(0xffffffffu, kv, j);
+                    pi = __shfl_xor_sync(0xffffffffu, iv, j);
+                }
+                const bool lower = (t & j) == 0;           // keep the min iff lower == up
+                if (lower == up ? pk < kv : pk > kv) { kv = pk; iv = pi; }
+            }
+        }
+        __syncthreads();                                   // wbox reuse at the next level
+    }
+    order[base + t] = iv;
+}
+
 }  // namespace
 
 // perm[k] = index of the k-th point in cell order (Hilbert curve over 64^3 cells).  pts: n points, `stride` floats apart.
@@ -197,6 +265,15 @@ cudaError_t spatial_order(const float *d_pts, int stride, int64_t n, int *d_perm
     cudaFreeAsync(cell, s);
     cudaFreeAsync(sums, s);
     return e;
+}
+
+// Refine a cell order into kd-tree leaves of 32 inside every full block of 1024 (see above).
+cudaError_t kd_refine(const float *d_pts, int stride, int64_t n, int *d_perm, cudaStream_t s) {
+    static_assert(kKdBlock == kSuper * kChunk, "a kd block is one superchunk");
+    if (n < kKdBlock) return cudaSuccess;
+    kd_chunks_kernel<<<(unsigned)(n / kKdBlock), kKdBlock, 0, s>>>(d_pts, stride, d_perm, n);
+    note_launches(1);
+    return cudaGetLastError();
 }
 
 }  // namespace rici
