@@ -263,6 +263,30 @@ def test_crss_count_mma_guard_and_fallback(rici, oracle_mod, big):
     assert np.array_equal(r.astype(np.uint32), oracle_mod.ranks(A, H))
 
 
+def test_crss_guard_edges_exact(rici, oracle_mod):
+    """The int8 guard at its edges: needle steps of exactly +-63 (largest -2 D_n that is s8; the
+    change mask and sum D_n^2 come from those bytes) and +-64 (first outside: SIMT fallback),
+    haystack steps of exactly +-15 (D_h^2 = 225, largest u8) and +-16 -- sparse, mixed with
+    rows that break 2:4; counts and ranks equal the oracle."""
+    rng = np.random.default_rng(63)
+    A = _rand_imgs(rng, 520, hi=4, density=0.03)
+    H = np.concatenate([A + (rng.random(A.shape) < 0.003).astype(np.uint16), _rand_imgs(rng, 300, hi=4, density=0.05)])
+    for q, (r, c, v) in enumerate([(5, 10, 63), (7, 40, 64), (30, 2, 63), (31, 60, 64)]):
+        A[q, r, c:] = v                                          # a +v step at c (and -v at 64 if c < 63)
+        A[q + 4, r, c] = v                                       # +v then -v: two steps of magnitude v
+    for q, (r, c, v) in enumerate([(9, 11, 15), (20, 33, 16), (40, 1, 15), (50, 62, 16)]):
+        H[100 + q, r, c] = v
+        H[200 + q, r, c:] = v
+    D = oracle_mod.crss_matrix(A, H)
+    thr = D[np.arange(A.shape[0]), rng.integers(0, H.shape[0], A.shape[0])].copy()
+    got = rici.rici_crss_count_below(_dev(A), _dev(H), torch.from_numpy(thr.view(np.int64)).to(DEV))
+    assert np.array_equal(got.cpu().numpy().astype(np.int64), (D < thr[:, None]).sum(1))
+    r = rici.rici_crss_search(_dev(A), _dev(H)).cpu().numpy()
+    assert np.array_equal(r.astype(np.uint32), oracle_mod.ranks(A, H))
+    d = rici.rici_crss_distances(_dev(A[:40]), _dev(H[:260])).cpu().numpy().view(np.uint64)
+    assert np.array_equal(d, D[:40, :260])
+
+
 def _band_copies(rng, A, rows, k):
     """Copies of needle images whose changes differ from the original only in `rows`."""
     out = A[rng.integers(0, A.shape[0], k)].copy()
