@@ -1,6 +1,7 @@
 """Small end-to-end run through every kernel (for compute-sanitizer): mesh staging, spatial
-sort, construction, thresholds, SIMT search (full + early exit), tensor-core search with the
-guard fallback, distances, pairs."""
+sort and kd chunk refinement, construction, thresholds, SIMT search (full + early exit),
+tensor-core search with the guard fallback (2- and 4-CTA clusters, one and two haystack tiles
+per unit, rank-mode prefix passes), distances, pairs."""
 import os
 import sys
 
@@ -24,6 +25,15 @@ r3 = rici.rici_crss_search(im[:300], h, early_exit=True)
 d = rici.rici_crss_distances(im[:40], h[:70])
 p = rici.rici_crss_pairs(im, h, torch.tensor([[0, 1], [5, 5]], dtype=torch.int64).cuda())
 r30 = rici.rici_crss_search(im30, im30)
+# a larger mesh: kd chunk refinement over several blocks, 4-CTA clusters with two tiles per
+# unit (>= 512 needles), and (RICI_SP_SIDE_FRAC) the side slice
+m2 = synth.bumpy_torus(80, 40, key=(8,))
+mesh2 = rici.rici_create_mesh(torch.from_numpy(m2.vertices).cuda(), torch.from_numpy(m2.indices).cuda())
+im2 = rici.rici_generate(mesh2, torch.from_numpy(m2.origins).cuda(), 0.3, 64)
+nee = im2[:700].clone()
+nee[1::2] = im2[(torch.arange(1, 700, 2, device="cuda") * 7 + 3) % im2.shape[0]]
+r4 = rici.rici_crss_search(nee, im2)
+r5 = rici.rici_crss_search(nee, im2, early_exit=True)
 torch.cuda.synchronize()
-assert torch.equal(r1, r2) and torch.equal(r1, r3)
-print("ok", int(r1.sum()), int(d.sum()), int(p.sum()), int(r30.sum()))
+assert torch.equal(r1, r2) and torch.equal(r1, r3) and torch.equal(r4, r5)
+print("ok", int(r1.sum()), int(d.sum()), int(p.sum()), int(r30.sum()), int(r4.sum()))
