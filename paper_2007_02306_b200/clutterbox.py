@@ -88,6 +88,8 @@ def run_scene(scene: int, levels, grid=(120, 60), box_side: float = 3.0, R: floa
     """One clutterbox run: returns {level: histogram} plus timing.  `generate(mesh, origins)` and
     `search(needles, haystack)` default to the CUDA library."""
     import synth
+    if generate is None and search is None and clutter is None:
+        return _run_scene_device(scene, levels, grid, box_side, R, N)
     if generate is None or search is None:
         import torch
 
@@ -132,6 +134,51 @@ def run_scene(scene: int, levels, grid=(120, 60), box_side: float = 3.0, R: floa
             cf = clutter(sc, tag, sc.origins[:n_ref])
             h["mean_clutter_fraction"] = float(np.mean(cf))
             h["clutter_rank_heatmap"] = clutter_rank_heatmap(cf, ranks)
+        h.update({"n_objects": lv, "n_scene_vertices": nv, "n_scene_triangles": nt,
+                  "comparisons": int(n_ref) * nv})
+        out["levels"][lv] = h
+    out["seconds"] = time.perf_counter() - t0
+    return out
+
+
+def _run_scene_device(scene: int, levels, grid, box_side: float, R: float, N: int):
+    """run_scene with the CUDA library, device-resident: the placed scene (vertices, indices,
+    oriented points) goes to the GPU once, and clutter level n is the prefix of the first n
+    objects -- the reference first (G11) -- so each level's mesh, origins and triangle tags are
+    slices of those buffers; one mesh per level serves construction and the Eq. 8 clutter
+    fraction.  Same outputs as the generic path (tests/test_clutterbox.py)."""
+    import synth
+    import torch
+
+    import paper_2007_02306_b200 as rici
+    levels = sorted(set(int(x) for x in levels))
+    objs = build_scene_objects(scene, max(levels), grid)
+    placed = synth.clutterbox(objs, key=(5, scene, 1000), box_side=box_side)
+    n_ref = objs[0].n_vertices
+    V = torch.from_numpy(placed.vertices).cuda()
+    T = torch.from_numpy(placed.indices).cuda()
+    O = torch.from_numpy(placed.origins).cuda()
+    tag_all = torch.zeros(placed.indices.shape[0], dtype=torch.uint8, device="cuda")
+    tag_all[: objs[0].n_triangles] = 1
+    t0 = time.perf_counter()
+    # {RD}: the reference object alone (vertex and triangle prefix of the placed scene)
+    m_ref = rici.rici_create_mesh(V[:n_ref], T[: objs[0].n_triangles])
+    rd = rici.rici_generate(m_ref, O[:n_ref], R, N)
+    m_ref.destroy()
+    out = {"scene": scene, "n_reference_vertices": n_ref, "levels": {}}
+    v_off = np.cumsum([0] + [o.n_vertices for o in objs])
+    t_off = np.cumsum([0] + [o.n_triangles for o in objs])
+    for lv in levels:
+        nv, nt = int(v_off[lv]), int(t_off[lv])
+        m = rici.rici_create_mesh(V[:nv], T[:nt])
+        cd = rici.rici_generate(m, O[:nv], R, N)            # {CD} of the combined mesh
+        ranks_d = rici.rici_crss_search(rd, cd, early_exit=True)   # rank mode (P:499)
+        cf_d = rici.rici_clutter_fraction(m, tag_all[:nt], O[:n_ref], R)   # f4: Eq. 8
+        m.destroy()
+        ranks, cf = ranks_d.cpu().numpy(), cf_d.cpu().numpy()
+        h = rank_histogram(ranks, nv)
+        h["mean_clutter_fraction"] = float(np.mean(cf))
+        h["clutter_rank_heatmap"] = clutter_rank_heatmap(cf, ranks)
         h.update({"n_objects": lv, "n_scene_vertices": nv, "n_scene_triangles": nt,
                   "comparisons": int(n_ref) * nv})
         out["levels"][lv] = h

@@ -39,6 +39,37 @@ def test_scene_protocol_cuda():
     assert out["levels"][4]["total"] == 64 * 32
 
 
+@pytest.mark.gpu
+def test_device_resident_scene_path_equals_generic():
+    """The device-resident harness path (scene uploaded once, levels as prefixes) gives the same
+    histograms, clutter fractions and heatmaps as the generic per-level path on the library."""
+    import torch
+    import paper_2007_02306_b200 as rici
+    R, N = 0.3, 64
+
+    def generate(mesh, origins):
+        m = rici.rici_create_mesh(torch.from_numpy(mesh.vertices).cuda(), torch.from_numpy(mesh.indices).cuda())
+        out = rici.rici_generate(m, torch.from_numpy(origins).cuda(), R, N)
+        m.destroy()
+        return out
+
+    def search(a, b):
+        return rici.rici_crss_search(a, b, early_exit=True).cpu().numpy()
+
+    def clutter(mesh, tag, origins):
+        m = rici.rici_create_mesh(torch.from_numpy(mesh.vertices).cuda(), torch.from_numpy(mesh.indices).cuda())
+        f = rici.rici_clutter_fraction(m, torch.from_numpy(tag).cuda(), torch.from_numpy(origins).cuda(), R)
+        m.destroy()
+        return f.cpu().numpy()
+
+    fast = run_scene(3, [1, 2, 5], grid=(40, 20))
+    slow = run_scene(3, [1, 2, 5], grid=(40, 20), generate=generate, search=search, clutter=clutter)
+    for lv in (1, 2, 5):
+        a, b = fast["levels"][lv], slow["levels"][lv]
+        assert a["counts"] == b["counts"] and a["clutter_rank_heatmap"] == b["clutter_rank_heatmap"]
+        assert a["mean_clutter_fraction"] == b["mean_clutter_fraction"]
+
+
 def test_heatmap_counts():
     from paper_2007_02306_b200.clutterbox import clutter_rank_heatmap
     h = clutter_rank_heatmap(np.array([0.0, 0.05, 0.5, 0.99, 1.0]), np.array([0, 1, 3, 2000, 0]), 10)
