@@ -44,7 +44,8 @@ def _load():
         lib.oracle_project.restype = None
         lib.oracle_segment.argtypes = [P, P, P, ctypes.c_double, P]
         lib.oracle_segment.restype = ctypes.c_int
-        lib.oracle_rici_generate.argtypes = [P, i64, P, i64, P, i64, ctypes.c_double, ctypes.c_int, P, P, P]
+        lib.oracle_rici_generate.argtypes = [P, i64, P, i64, P, i64, ctypes.c_double, ctypes.c_int, P, P, P,
+                                             ctypes.c_double]
         lib.oracle_rici_generate.restype = None
         lib.oracle_rici_definition.argtypes = [P, i64, P, i64, P, i64, ctypes.c_double, ctypes.c_int, P]
         lib.oracle_rici_definition.restype = None
@@ -109,12 +110,13 @@ def _mesh_args(vertices, indices, origins):
 
 
 def rici_generate(vertices, indices, origins, support_radius: float, n_bins: int,
-                  fragile: bool = False, exact: bool = False):
+                  fragile: bool = False, exact: bool = False, tau_rel: float = 1e-5):
     """Paper algorithm in double on the float32 inputs.
 
     Returns uint16 images [n, N, N] saturated at 65535 (G9) -- or the exact
     uint32 counts when ``exact`` -- plus, when ``fragile``, a bool mask of the
-    pixels whose count changes under a tau = 1e-5*R displacement of the circle,
+    pixels whose count changes under a tau = tau_rel*R displacement of the circle
+    (default 1e-5, the north-star rule),
     and stats {pairs_in_slab, segments}.
     """
     v, t, o = _mesh_args(vertices, indices, origins)
@@ -124,7 +126,7 @@ def rici_generate(vertices, indices, origins, support_radius: float, n_bins: int
     stats = np.zeros(2, dtype=np.int64)
     _load().oracle_rici_generate(_ptr(v), v.shape[0], _ptr(t), t.shape[0], _ptr(o), n,
                                  float(support_radius), N, _ptr(counts),
-                                 _ptr(fr) if fragile else None, _ptr(stats))
+                                 _ptr(fr) if fragile else None, _ptr(stats), float(tau_rel))
     img = counts if exact else np.minimum(counts, 65535).astype(np.uint16)
     res = {"images": img, "pairs_in_slab": int(stats[0]), "segments": int(stats[1])}
     if fragile:

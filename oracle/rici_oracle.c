@@ -225,11 +225,17 @@ static void image_counts(const frame_t *f, const float *vertices, const int32_t 
 
 /* counts_out: n*N*N exact counts (uint32), row = beta ascending, col = alpha ascending.
  * fragile_out (optional): 1 where the count changes when the circle is moved by
- * up to tau = 1e-5*R in beta and/or rho (the north-star attribution rule).
+ * tau = tau_rel*R in beta and/or rho: the 8 displacements (a*tau, b*tau), a,b in
+ * {-1,0,1}, not both 0.  tau_rel = 1e-5 is the north-star attribution rule ("an
+ * intersection within 1e-5 relative of a bin or layer edge"); this is the
+ * perturbation reading of DESIGN.md section 2: a pixel whose count is the same at
+ * every displacement is NOT fragile even if a decision there is tied (e.g. a
+ * circle through an edge shared by two triangles: either triangle counts it).
  * stats (optional, int64[2]): {pairs whose beta-extent meets the image, segments}. */
 EXPORT void oracle_rici_generate(const float *vertices, int64_t nv, const int32_t *indices,
                                  int64_t nt, const float *origins, int64_t n, double R, int N,
-                                 uint32_t *counts_out, uint8_t *fragile_out, int64_t *stats) {
+                                 uint32_t *counts_out, uint8_t *fragile_out, int64_t *stats,
+                                 double tau_rel) {
     (void)nv;
     int64_t sp = 0, ss = 0;
 #pragma omp parallel for schedule(dynamic, 1) reduction(+ : sp, ss)
@@ -245,7 +251,7 @@ EXPORT void oracle_rici_generate(const float *vertices, int64_t nv, const int32_
             uint8_t *fr = fragile_out + i * (int64_t)N * N;
             memset(fr, 0, (size_t)N * N);
             uint32_t *alt = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)N * N);
-            const double tau = 1e-5 * R;
+            const double tau = tau_rel * R;
             for (int a = -1; a <= 1; ++a)
                 for (int b = -1; b <= 1; ++b) {
                     if (a == 0 && b == 0) continue;

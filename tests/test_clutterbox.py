@@ -85,3 +85,55 @@ def test_scene_with_clutter_fraction_oracle(oracle_mod):
                     clutter=lambda m, tag, o: oracle_mod.clutter_fraction(m.vertices, m.indices, tag, o, R)[0])
     assert out["levels"][1]["mean_clutter_fraction"] == 0.0
     assert np.array(out["levels"][2]["clutter_rank_heatmap"]["counts"]).sum() == out["n_reference_vertices"]
+
+
+@pytest.mark.gpu
+def test_scene_cuda_against_oracle(oracle_mod):
+    """f2 against the oracle: the harness runs on CUDA; at every clutter level the
+    oracle recounts every rank from the GPU-made {RD} and {CD} (bit-exact), so the
+    level's histogram is the oracle's; a sample of {RD} and {CD} images is checked against the
+    oracle's construction under the parity rule; the Eq. 8 fractions against the oracle's."""
+    import torch
+    import paper_2007_02306_b200 as rici
+    R, N = 0.3, 64
+    made, searched = [], []
+
+    def generate(mesh, origins):
+        m = rici.rici_create_mesh(torch.from_numpy(mesh.vertices).cuda(), torch.from_numpy(mesh.indices).cuda())
+        out = rici.rici_generate(m, torch.from_numpy(origins).cuda(), R, N)
+        m.destroy()
+        made.append((mesh, origins, out.cpu().numpy().view(np.uint16)))
+        return out
+
+    def search(a, b):
+        r = rici.rici_crss_search(a, b, early_exit=True).cpu().numpy()
+        searched.append((a.cpu().numpy().view(np.uint16), b.cpu().numpy().view(np.uint16), r))
+        return r
+
+    def clutter(mesh, tag, origins):
+        m = rici.rici_create_mesh(torch.from_numpy(mesh.vertices).cuda(), torch.from_numpy(mesh.indices).cuda())
+        f = rici.rici_clutter_fraction(m, torch.from_numpy(tag).cuda(), torch.from_numpy(origins).cuda(), R)
+        m.destroy()
+        want = oracle_mod.clutter_fraction(mesh.vertices, mesh.indices, tag, origins, R)[0]
+        assert np.abs(f.cpu().numpy().astype(np.float64) - want).max() <= 2e-4
+        return f.cpu().numpy()
+
+    levels = [1, 3, 6]
+    out = run_scene(4, levels, grid=(48, 24), generate=generate, search=search, clutter=clutter)
+    assert len(searched) == len(levels)
+    for lv, (rd, cd, ranks) in zip(levels, searched):
+        want = oracle_mod.ranks(rd, cd)
+        assert np.array_equal(ranks.astype(np.uint32), want)
+        assert out["levels"][lv]["counts"] == rank_histogram(want, cd.shape[0])["counts"]
+    assert out["levels"][6]["rank0_fraction"] < 1.0 or out["levels"][6]["mean_clutter_fraction"] > 0
+    rng = np.random.default_rng(0)
+    for mesh, origins, imgs in made:
+        k = min(200, imgs.shape[0])
+        idx = np.sort(rng.choice(imgs.shape[0], k, replace=False))
+        ref = oracle_mod.rici_generate(mesh.vertices, mesh.indices, origins[idx], R, N, fragile=True)
+        diff = imgs[idx] != ref["images"]
+        assert not (diff & ~ref["fragile"]).any() and diff.mean() <= 1e-4
+    # and the device-resident default path gives the same histograms
+    fast = run_scene(4, levels, grid=(48, 24))
+    for lv in levels:
+        assert fast["levels"][lv]["counts"] == out["levels"][lv]["counts"]

@@ -43,6 +43,21 @@ def _assert_parity(gpu, ref, max_frac=1e-4):
     return int(diff.sum())
 
 
+def _parity_sampled(oracle_mod, g, mesh, origins, R, N, max_frac=1e-4):
+    """The parity rule on a sample of images, with the oracle's fragility stencil (9 runs of
+    the algorithm per image) evaluated only on the images that differ.  Returns n_diff."""
+    ref = oracle_mod.rici_generate(mesh.vertices, mesh.indices, origins, R, N)
+    diff = g != ref["images"]
+    n_diff = int(diff.sum())
+    bad = np.nonzero(diff.reshape(diff.shape[0], -1).any(1))[0]
+    if bad.size:
+        fr = oracle_mod.rici_generate(mesh.vertices, mesh.indices, origins[bad], R, N, fragile=True)["fragile"]
+        n_bad = int((diff[bad] & ~fr).sum())
+        assert n_bad == 0, f"{n_bad} non-attributable differing pixels in {bad.size} images"
+    assert n_diff <= max_frac * diff.size, f"{n_diff} differing pixels ({n_diff / diff.size:.2e})"
+    return n_diff
+
+
 def test_c1_icosphere(rici, oracle_mod):
     cfg = synth.config_c1()
     g = _gen(rici, cfg["mesh"], cfg["origins"], cfg["R"], cfg["N"])
@@ -71,6 +86,28 @@ def test_cube_and_tetra_closed_forms(rici, oracle_mod):
     o = np.array([[1, 1, 1, s, s, s]], np.float32)
     g = _gen(rici, t, o, 1.0, 64)
     assert g.sum() == 1080
+
+
+def test_h3_face_diagonal_ties_exact(rici, oracle_mod):
+    """H3': the cube corner with S_n = +z puts 32 pixels exactly on a face diagonal shared by
+    two triangles.  The count there (2) is locally constant, so the oracle does not flag it and
+    the GPU must match every pixel exactly."""
+    c = synth.cube()
+    o = np.array([[1, 1, 1, 0, 0, 1]], np.float32)
+    g = _gen(rici, c, o, 1.0, 64)
+    ref = oracle_mod.rici_generate(c.vertices, c.indices, o, 1.0, 64, fragile=True)
+    assert not ref["fragile"].any()
+    assert np.array_equal(g, ref["images"])
+
+
+@pytest.mark.parametrize("k", [0.5, -0.5, 2.0, -2.0])
+def test_tau_width_cases_exact(rici, oracle_mod, k):
+    """The tau-width pins of tests/test_oracle_rici.py (one decision k*tau from a layer edge, a
+    |C| edge and a |E| edge): the float32 path resolves even the k = +-0.5 ties exactly."""
+    from test_oracle_rici import layer_edge_triangle, double_range_plane, single_range_plane, _O_UP
+    for m in (layer_edge_triangle(k), double_range_plane(k), single_range_plane(k)):
+        g = _gen(rici, m, _O_UP, 1.0, 64)
+        assert np.array_equal(g, oracle_mod.rici_generate(m.vertices, m.indices, _O_UP, 1.0, 64)["images"])
 
 
 @pytest.mark.parametrize("N", [2, 8, 30, 64, 100, 128])
@@ -108,6 +145,14 @@ def test_adversarial(rici, oracle_mod, case):
     if case == "grid_soup":
         assert ref["fragile"].mean() > 5e-3
         n_diff = _assert_parity(g, ref, max_frac=1.0)
+        # every differing pixel must be an EXACT tie: flagged by the same stencil at
+        # tau = 1e-12 R, far below float32 resolution (~6e-8 R), i.e. a decision whose double-
+        # precision margin is zero up to rounding -- where FP32 and FP64 may both be right (G16)
+        tie = oracle_mod.rici_generate(m.vertices, m.indices, o, R, 64, fragile=True, tau_rel=1e-12)["fragile"]
+        diff = g != ref["images"]
+        assert not (diff & ~tie).any(), f"{int((diff & ~tie).sum())} of {n_diff} differing pixels are not exact ties"
+        print(f"grid_soup: {n_diff} differing pixels, {int(tie.sum())} exact-tie pixels, "
+              f"{int(ref['fragile'].sum())} fragile of {diff.size}")
         assert n_diff <= 0.1 * ref["fragile"].sum()
     else:
         _assert_parity(g, ref)
@@ -141,10 +186,9 @@ def test_c2_sampled(rici, oracle_mod):
     m = cfg["mesh"]
     g = _gen(rici, m, cfg["origins"], cfg["R"], cfg["N"])
     rng = np.random.default_rng(0)
-    idx = np.sort(rng.choice(m.n_vertices, 600, replace=False))
+    idx = np.sort(rng.choice(m.n_vertices, 2000, replace=False))   # >= 2,000
     idx[-1] = m.n_vertices - 1                               # the ragged tail
-    ref = oracle_mod.rici_generate(m.vertices, m.indices, cfg["origins"][idx], cfg["R"], cfg["N"], fragile=True)
-    _assert_parity(g[idx], ref)
+    _parity_sampled(oracle_mod, g[idx], m, cfg["origins"][idx], cfg["R"], cfg["N"])
     # property at full size: closed surface -> even counts except fragile pixels (sampled above)
     assert (g % 2 == 1).mean() < 1e-4
 
@@ -400,10 +444,9 @@ def test_c3_clutterbox_full_size_sampled(rici, oracle_mod):
     m = cfg["mesh"]
     assert m.n_triangles == 998_560 and m.n_vertices == 499_280
     g = _gen(rici, m, cfg["origins"], cfg["R"], cfg["N"])
-    idx = np.sort(np.random.default_rng(3).choice(m.n_vertices, 96, replace=False))
+    idx = np.sort(np.random.default_rng(3).choice(m.n_vertices, 2000, replace=False))
     idx[-1] = m.n_vertices - 1
-    ref = oracle_mod.rici_generate(m.vertices, m.indices, cfg["origins"][idx], cfg["R"], cfg["N"], fragile=True)
-    _assert_parity(g[idx], ref)
+    _parity_sampled(oracle_mod, g[idx], m, cfg["origins"][idx], cfg["R"], cfg["N"])
 
 
 @pytest.mark.slow
@@ -419,11 +462,19 @@ def test_c4_full_size_ranks_sampled(rici, oracle_mod):
     hd = rici.rici_generate(hm, torch.from_numpy(sc.origins).to(DEV), cfg["R"], cfg["N"])
     ranks = rici.rici_crss_search(nd, hd).cpu().numpy()
     assert ranks.shape == (100_352,) and (ranks >= 0).all() and (ranks < 1_003_520).all()
-    idx = np.random.default_rng(4).choice(100_352, 8, replace=False)
+    idx = np.random.default_rng(4).choice(100_352, 64, replace=False)       # 64 needles
+    idx[0] = 100_351                                                         # the last needle
     n = nd.cpu().numpy().view(np.uint16)
     h = hd.cpu().numpy().view(np.uint16)
     thr = np.array([oracle_mod.crss(n[i], h[i]) for i in idx], np.uint64)
     assert np.array_equal(ranks[idx].astype(np.uint32), oracle_mod.count_below(n[idx], h, thr))
+    # the 2M-triangle construction itself, under the parity rule: 500 haystack images (incl. the
+    # last) and 500 needle images (the reference alone)
+    hi = np.sort(np.random.default_rng(5).choice(sc.n_vertices, 500, replace=False))
+    hi[-1] = sc.n_vertices - 1
+    _parity_sampled(oracle_mod, h[hi], sc, sc.origins[hi], cfg["R"], cfg["N"])
+    ni = np.sort(np.random.default_rng(6).choice(ref.n_vertices, 500, replace=False))
+    _parity_sampled(oracle_mod, n[ni], ref, ref.origins[ni], cfg["R"], cfg["N"])
 
 
 # ------------------------------------------------------------------ f4: Eq. 8 clutter fraction

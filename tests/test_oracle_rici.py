@@ -71,6 +71,17 @@ def test_h3_cube_face_diagonal_ties(oracle_mod):
     r = oracle_mod.rici_generate(c.vertices, c.indices, o, R, N, fragile=True)
     img = r["images"][0]
     assert (img[:32] == 2).all() and (img[32:] == 0).all()
+    # The 32 pixels with r + c = 31 are exact ties: rho_c = depth, so the circle passes through
+    # a point of a face diagonal, the edge shared by the face's two triangles.  Under the
+    # perturbation reading they are NOT fragile: at every displacement of
+    # up to tau the circle still crosses that face exactly once (in one triangle or the other),
+    # so the count 2 is locally constant and there is nothing to attribute.  A margin reading
+    # (|rho_c - |E|| <= tau) would flag them; this reading is stricter, so a GPU path must get
+    # them exactly right.
+    ties = np.add.outer(np.arange(64), np.arange(64)) == 31
+    assert ties[:32].sum() == 32
+    assert not r["fragile"].any()
+    assert (img[ties] == 2).all()
 
 
 def test_h4_tetrahedron_apex_closed_form(oracle_mod):
@@ -176,3 +187,88 @@ def test_rigid_invariance_dyadic(oracle_mod):
     moved = oracle_mod.rici_generate(v2, m.indices, o2, 0.3, 64, fragile=True)
     ok = ~(base["fragile"] | moved["fragile"])
     assert np.array_equal(base["images"][ok], moved["images"][ok])
+
+
+# --------------------------------------------------------------------------------------------
+# The width of the attribution rule: tau = 1e-5 * R (north_star: "an intersection within 1e-5
+# relative of a bin or layer edge").  Each case puts ONE decision at a known distance k*tau
+# from a bin or layer edge: |k| = 0.5 must be flagged, |k| = 2 must not, so a stencil that is
+# too wide (>= 2 tau) or too narrow (< 0.5 tau) fails.  Float32 inputs sit within 1e-8 of the
+# intended values (<= 0.002 tau).
+TAU_R, TAU_N = 1.0, 64
+_O_UP = np.array([[0, 0, 0, 0, 0, 1]], np.float32)
+
+
+def _row_beta(r):
+    return (r + 0.5) * TAU_R / TAU_N - TAU_R / 2
+
+
+def _col_rho(c):
+    return (c + 0.5) * TAU_R / TAU_N
+
+
+def layer_edge_triangle(k, r=40, a=0.3137):
+    """A triangle in the vertical plane x = a whose lowest edge (both bottom vertices) lies
+    k*tau above the centre of layer r: layer membership z_min <= beta_r < z_max (G5) flips
+    under a beta displacement iff |k| < 1."""
+    z0 = _row_beta(r) + k * 1e-5 * TAU_R
+    V = np.array([[a, -0.4, z0], [a, 0.4, z0], [a, 0.0, z0 + 0.2]], np.float32)
+    return synth.Mesh(V, np.array([[0, 1, 2]], np.int32), np.zeros((3, 3), np.float32))
+
+
+def double_range_plane(k, c=30):
+    """The plane x = a with a = rho_c + k*tau: every slice has |C| = a and the double range
+    [|C|, min|E|) of column c flips under a rho displacement iff |k| < 1."""
+    a = _col_rho(c) + k * 1e-5 * TAU_R
+    return synth.quad([[a, -5, -5], [a, 5, -5], [a, 5, 5], [a, -5, 5]])
+
+
+def single_range_plane(k, c=25):
+    """A strip of the plane y = 0 covering x in [0.1, e) with e = rho_c + k*tau: the single
+    range [min|E|, max|E|) = [0.1, e) of column c flips under a rho displacement iff |k| < 1."""
+    e = _col_rho(c) + k * 1e-5 * TAU_R
+    return synth.quad([[0.1, 0, -5], [e, 0, -5], [e, 0, 5], [0.1, 0, 5]])
+
+
+@pytest.mark.parametrize("k", [0.5, -0.5])
+def test_tau_width_layer_edge_flagged(oracle_mod, k):
+    m = layer_edge_triangle(k)
+    r = oracle_mod.rici_generate(m.vertices, m.indices, _O_UP, TAU_R, TAU_N, fragile=True)
+    fr, img = r["fragile"][0], r["images"][0]
+    assert set(np.nonzero(fr.any(1))[0]) == {40}           # exactly the tied layer
+    # the flagged pixels are the columns the slice at beta_40 (+-tau) reaches: 2 on the double
+    # range [a, sqrt(a^2 + y^2)) of the plane's slice
+    cols = np.nonzero(fr[40])[0]
+    assert len(cols) > 0 and (_col_rho(cols) >= 0.3137).all()
+    assert (img[40] == (2 * fr[40] if k < 0 else 0)).all()  # row 40 is counted iff z_min <= beta_40
+
+
+@pytest.mark.parametrize("k", [2.0, -2.0])
+def test_tau_width_layer_edge_not_flagged(oracle_mod, k):
+    m = layer_edge_triangle(k)
+    r = oracle_mod.rici_generate(m.vertices, m.indices, _O_UP, TAU_R, TAU_N, fragile=True)
+    assert not r["fragile"].any()
+    assert r["images"][0][40].any() == (k < 0)
+    # ... but a stencil of 3 tau would reach the edge: the rule's width is what decides
+    r3 = oracle_mod.rici_generate(m.vertices, m.indices, _O_UP, TAU_R, TAU_N, fragile=True, tau_rel=3e-5)
+    assert set(np.nonzero(r3["fragile"][0].any(1))[0]) == {40}
+
+
+@pytest.mark.parametrize("plane,c", [(double_range_plane, 30), (single_range_plane, 25)])
+@pytest.mark.parametrize("k", [0.5, -0.5, 2.0, -2.0])
+def test_tau_width_radius_edge(oracle_mod, plane, c, k):
+    m = plane(k, c)
+    r = oracle_mod.rici_generate(m.vertices, m.indices, _O_UP, TAU_R, TAU_N, fragile=True)
+    fr, img = r["fragile"][0], r["images"][0]
+    if abs(k) < 1:
+        assert set(np.nonzero(fr.any(0))[0]) == {c}        # exactly the tied column ...
+        assert fr[:, c].all()                              # ... in every row the plane spans
+    else:
+        assert not fr.any()
+        r3 = oracle_mod.rici_generate(m.vertices, m.indices, _O_UP, TAU_R, TAU_N, fragile=True, tau_rel=3e-5)
+        assert set(np.nonzero(r3["fragile"][0].any(0))[0]) == {c}
+    # the undisplaced count at column c follows the side of the edge the bin centre is on
+    if plane is double_range_plane:
+        assert (img[:, c] == (2 if k < 0 else 0)).all()     # rho_c >= |C| = rho_c + k tau iff k <= 0
+    else:
+        assert (img[:, c] == (1 if k > 0 else 0)).all()     # rho_c < e = rho_c + k tau iff k > 0
