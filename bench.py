@@ -1,14 +1,21 @@
 """Benchmark of the RICI hot path (arXiv 2007.02306) on B200.
 
-One step = one pass of the whole hot path over the C2 workload (BASELINE.json configs[1]):
-  a1     rici_create_mesh   bumpy torus 264x132, T=69,696 triangles
-  a2-a8  rici_generate      RICI 64x64 at all V=34,848 vertices, R=0.3
-  a9-a12 rici_crss_search   every image as a needle against all images (self-search,
-                            correspondence i <-> i): 34,848^2 = 1.21e9 CRSS comparisons
-value = images (generated and ranked) per second for the whole job.  At N>1 GPUs (weak
-scaling) each rank adds its own C2-sized object: rank r generates object r's images (its
-haystack shard); the needles are rank 0's images (broadcast); thresholds and counts are
-all-reduced over NCCL (paper_2007_02306_b200.dist).
+One step = one pass of the whole hot path over the C4 workload (BASELINE.json configs[3],
+"CRSS rank search: 100k needle images vs 1M haystack images"):
+  a1     rici_create_mesh   the reference object alone (448x224 torus, T=200,704) and the
+                            clutterbox scene (reference placed first + 9 clutter objects,
+                            T=2,007,040)
+  a2-a8  rici_generate      needles: RICI 64x64 at the 100,352 reference vertices;
+                            haystack: RICI 64x64 at all 1,003,520 scene vertices (R=0.3)
+  a9-a12 rici_crss_search   full mode: every needle against every haystack image,
+                            1.007e11 CRSS comparisons, rank of the true correspondence i <-> i
+value = images generated (and ranked) per second of the whole step; comparisons_per_s rides
+along.  Extra keys: C3 construction (configs[2]), the C2 step (configs[1]).
+
+At N > 1 GPUs the SAME scene is split (strong scaling): rank 0 builds the meshes
+and broadcasts them (NCCL), every rank generates its contiguous block of the scene's oriented
+points (its haystack shard) and of the reference's (all-gathered into the needle set), then
+search_sharded: thresholds by the owner of h_i + all_reduce(MAX), local counts + all_reduce(SUM).
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 """
@@ -17,6 +24,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import subprocess
 import sys
 import threading
 import time
@@ -31,11 +39,29 @@ PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 SMS = 148
 LANES_PER_SM = 128          # FP32/INT32 lanes per SM
 CRSS_OPS_PER_TERM = 3       # D_h difference, (D_n - D_h), multiply-accumulate
+K_FEAT = 2 * 4096           # int8 feature length per image
+WORKLOAD = ("C4 (BASELINE configs[3]): needles = RICI 64x64 at the 100,352 vertices of a 448x224 "
+            "bumpy torus (T=200,704) alone; haystack = RICI 64x64 at all 1,003,520 vertices of a "
+            "10-object clutterbox (reference placed first, T=2,007,040), R=0.3; full-mode CRSS "
+            "search 100,352 x 1,003,520 = 1.007e11 comparisons, ranks of i <-> i")
+
+
+def ncu_metric(kernel, metric):
+    """A metric of `kernel` from the newest committed ncu summary (profiles/r*_ncu_summary.txt)."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_summary.txt")), reverse=True):
+        cur = None
+        for line in open(path):
+            if line.startswith("== "):
+                cur = line[3:].strip()
+            elif cur and cur.split("<")[0] == kernel and line.strip().startswith(metric + " ="):
+                return float(line.split("=")[1].split()[0]), os.path.relpath(path, ROOT)
+    return None, None
 
 
 def ncu_traffic(kernel):
     """dram__bytes_read.sum + dram__bytes_write.sum of `kernel` per launch, from the newest
-    committed `ncu --set full` summary under profiles/ (r1*_ncu_summary.txt); None if absent."""
+    committed `ncu --set full` summary under profiles/; None if absent."""
     import glob
     scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
     for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_summary.txt")), reverse=True):
@@ -53,31 +79,30 @@ def ncu_traffic(kernel):
     return None, None
 
 
-def ncu_metric(kernel, metric):
-    """A metric of `kernel` from the newest committed ncu summary (profiles/r*_ncu_summary.txt)."""
-    import glob
-    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_summary.txt")), reverse=True):
-        cur = None
-        for line in open(path):
-            if line.startswith("== "):
-                cur = line[3:].strip()
-            elif cur and cur.split("<")[0] == kernel and line.strip().startswith(metric + " ="):
-                return float(line.split("=")[1].split()[0]), os.path.relpath(path, ROOT)
-    return None, None
-
-
 def peaks():
     try:
         with open(PEAKS_PATH) as f:
-            p = json.load(f)
-        return p, "measured"
+            return json.load(f), "measured"
     except Exception:
-        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def host_cpu():
+    """nproc and the lscpu model name of this host."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return {"nproc": os.cpu_count(), "model": model}
 
 
 class ClockSampler:
-    """SM clock + throttle reasons sampled DURING the timed region: NVML polled every ~2 ms from
-    a thread (the timed region is only tens of ms), nvidia-smi as a fallback."""
+    """SM clock + throttle reasons sampled DURING the timed region (NVML polled every ~2 ms)."""
 
     REASONS = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
                "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
@@ -126,99 +151,199 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.sm), "source": "nvml, 2 ms polling"}
 
 
-# ----------------------------------------------------------------------------- workload
-def workload(rank: int):
-    import synth
-    cfg = synth.config_c2() if rank == 0 else {
-        **synth.config_c2(), "mesh": synth.bumpy_torus(264, 132, key=(2, rank, 0))}
-    if rank != 0:
-        cfg["origins"] = cfg["mesh"].origins
-    return cfg
-
-
-def cpu_baseline(cfg, budget_s: float = 20.0):
-    """The oracle as it stands on a bounded sample of the C2 step: generate a sample of the
-    images and run CRSS of sampled needles against a sample of the haystack; extrapolate the
-    step's time (n * t_image + n^2 * t_comparison) and report images/s of the step."""
+# ----------------------------------------------------------------------------- oracle legs
+def oracle_c4_sample(cfg, k_img: int, nn_cmp: int, haystack=None, nh_cmp: int | None = None,
+                     needles=None):
+    """Time the oracle as it stands (oracle/, all host cores) on a sample of the C4 step and
+    extrapolate the step:  t_step = n_scene*t_scene_image + n_ref*t_ref_image + n_ref*n_scene*t_cmp.
+    k_img scene and k_img reference images are generated by the oracle; CRSS runs nn_cmp
+    needles against `haystack` (the full GPU-made haystack for the N=1 cpu_baseline, BASELINE.md
+    section 3: 64 needles x 1,003,520) or, without one, the oracle's own sample images tiled to
+    nh_cmp (the oracle's Eq. 7 loop costs the same for any uint16 input)."""
     import oracle
-    m = cfg["mesh"]
-    n = m.n_vertices
+    ref, sc, R, N = cfg["reference"], cfg["scene"], cfg["R"], cfg["N"]
     rng = np.random.default_rng(0)
-    k_img = 512
-    idx = np.sort(rng.choice(n, k_img, replace=False))
+    si = np.sort(rng.choice(sc.n_vertices, k_img, replace=False))
+    ri = np.sort(rng.choice(ref.n_vertices, k_img, replace=False))
     t0 = time.perf_counter()
-    imgs = oracle.rici_generate(m.vertices, m.indices, cfg["origins"][idx], cfg["R"], cfg["N"])["images"]
-    t_gen = time.perf_counter() - t0
-    per_img = t_gen / k_img
-    # CRSS: needles x haystack from the generated sample (the oracle's dense loop cost is
-    # data independent); scale the pair count to ~budget/2 seconds
-    nn_s, nh_s = 32, k_img
+    rs = oracle.rici_generate(sc.vertices, sc.indices, sc.origins[si], R, N)
+    t_scene = (time.perf_counter() - t0) / k_img
     t0 = time.perf_counter()
-    oracle.crss_matrix(imgs[:nn_s], imgs[:nh_s])
+    rr = oracle.rici_generate(ref.vertices, ref.indices, ref.origins[ri], R, N)
+    t_ref = (time.perf_counter() - t0) / k_img
+    if needles is None:
+        needles = rr["images"][np.arange(nn_cmp) % k_img]
+        thr_src = rs["images"][np.arange(nn_cmp) % k_img]
+    else:
+        idx = np.sort(rng.choice(needles.shape[0], nn_cmp, replace=False))
+        needles = needles[idx]
+        thr_src = haystack[idx]
+    if haystack is None:
+        haystack = rs["images"][np.arange(nh_cmp) % k_img]
+    thr = np.array([oracle.crss(needles[i], thr_src[i]) for i in range(nn_cmp)], np.uint64)
+    t0 = time.perf_counter()
+    oracle.count_below(needles, haystack, thr)
     t_c = time.perf_counter() - t0
-    reps = max(1, int((budget_s / 2) / max(t_c, 1e-3)))
-    t0 = time.perf_counter()
-    for _ in range(reps):
-        oracle.crss_matrix(imgs[:nn_s], imgs[:nh_s])
-    t_c = (time.perf_counter() - t0) / reps
-    per_cmp = t_c / (nn_s * nh_s)
-    t_step = n * per_img + float(n) * n * per_cmp
-    return {"value": n / t_step, "unit": "images/s", "cores": oracle.num_threads(), "kind": "oracle",
-            "sample": (f"oracle rici_generate of {k_img} sampled C2 images ({t_gen:.2f} s) + "
-                       f"{reps}x oracle CRSS {nn_s}x{nh_s} ({t_c:.3f} s each); step time "
-                       f"extrapolated as n*t_image + n^2*t_comparison for n={n}"),
-            "t_image_s": per_img, "t_comparison_s": per_cmp, "t_step_s": t_step}
-
-
-def segments_per_pair(cfg, k: int = 96) -> float:
-    """S/P for the paper-literal construction work W = 43 P + 40 S + 3 N^2 n,
-    from the oracle's segment counter on a fixed sample of images."""
-    import oracle
-    m = cfg["mesh"]
-    idx = np.linspace(0, m.n_vertices - 1, k).astype(np.int64)
-    r = oracle.rici_generate(m.vertices, m.indices, cfg["origins"][idx], cfg["R"], cfg["N"])
-    return r["segments"] / float(k * m.n_triangles)
+    t_cmp = t_c / (nn_cmp * haystack.shape[0])
+    n_s, n_r = sc.n_vertices, ref.n_vertices
+    t_step = n_s * t_scene + n_r * t_ref + float(n_r) * n_s * t_cmp
+    spp = rs["segments"] / float(k_img * sc.n_triangles)
+    spp_ref = rr["segments"] / float(k_img * ref.n_triangles)
+    cpu = host_cpu()
+    return {"value": (n_s + n_r) / t_step, "unit": "images/s", "cores": oracle.num_threads(),
+            "kind": "oracle", "cpu_model": cpu["model"], "nproc": cpu["nproc"],
+            "sample": (f"oracle rici_generate of {k_img} sampled C4 scene images ({t_scene * k_img:.2f} s) and "
+                       f"{k_img} reference images ({t_ref * k_img:.2f} s); oracle count_below of {nn_cmp} needles "
+                       f"x {haystack.shape[0]} haystack images ({t_c:.2f} s); step time EXTRAPOLATED as "
+                       f"n_scene*t_scene_image + n_ref*t_ref_image + n_ref*n_scene*t_comparison"),
+            "extrapolated": True,
+            "t_scene_image_s": t_scene, "t_ref_image_s": t_ref, "t_comparison_s": t_cmp, "t_step_s": t_step,
+            "comparisons_per_s": 1.0 / t_cmp, "segments_per_pair": spp, "segments_per_pair_ref": spp_ref}
 
 
 def run_reference(args):
-    """--impl reference: the oracle timed as it stands on the host cores (rank 0 only)."""
+    """--impl reference: the oracle timed as it stands on the host cores (rank 0 only); each step
+    is a bounded sample of the C4 step, extrapolated to the whole step (labelled)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    cfg = workload(0)
-    n = cfg["mesh"].n_vertices
+    import synth
+    cfg = synth.config_c4()
+    n = cfg["scene"].n_vertices + cfg["reference"].n_vertices
     for _ in range(args.warmup):
-        cpu_baseline(cfg, budget_s=2.0)
-    vals = []
-    cb = None
+        oracle_c4_sample(cfg, 8, 16, nh_cmp=4096)
+    vals, cb = [], None
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        cb = cpu_baseline(cfg, budget_s=6.0)
+        cb = oracle_c4_sample(cfg, 16, 64, nh_cmp=16384)
         vals.append(cb["t_step_s"])
     wall = time.perf_counter() - t0
     t_step = float(np.mean(vals))
     value = n / t_step
-    cbl = {k: cb[k] for k in ("unit", "cores", "kind", "sample")}
+    cbl = {k: cb[k] for k in ("unit", "cores", "kind", "sample", "cpu_model", "nproc", "extrapolated")}
     cbl["value"] = value
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "images/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64/i64", "data": "synthetic",
-            "config": {"workload": "C2: bumpy torus 264x132 (T=69,696), RICI 64x64 at all 34,848 "
-                                   "vertices, R=0.3, CRSS self-search 34,848 x 34,848",
-                       "bench_wall_s": wall},
+            "ms_per_step": t_step * 1e3, "ms_per_step_extrapolated": True,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64/i64",
+            "data": "synthetic",
+            "comparisons_per_s": cb["comparisons_per_s"],
+            "config": {"workload": WORKLOAD, "bench_wall_s": wall,
+                       "note": "each timed step runs a bounded oracle sample; ms_per_step is extrapolated"},
             "cpu_baseline": cbl,
             "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
 
 # ----------------------------------------------------------------------------- GPU arm
+def _bcast_mesh_arrays(arrays, dev, world, rank):
+    """Rank 0's host arrays -> device tensors on every rank (NCCL broadcast; the mesh is
+    replicated)."""
+    import torch
+    import torch.distributed as dist
+    out = []
+    for a in arrays:
+        if world == 1:
+            out.append(torch.from_numpy(a).to(dev))
+            continue
+        meta = [a.shape if rank == 0 else None, str(a.dtype) if rank == 0 else None]
+        dist.broadcast_object_list(meta, 0)
+        t = torch.from_numpy(a).to(dev) if rank == 0 else torch.empty(meta[0], dtype=getattr(torch, meta[1]),
+                                                                      device=dev)
+        dist.broadcast(t, 0)
+        out.append(t)
+    return out
+
+
+def extra_c3(rici, torch, dev, stream, flush, reps=3):
+    """C3 (BASELINE configs[2]) construction: 10-object clutterbox, 998,560 triangles, RICI at
+    all 499,280 vertices.  Mesh staging + rici_generate, device-resident, CUDA events."""
+    import synth
+    cfg = synth.config_c3()
+    m = cfg["mesh"]
+    v, t, o = (torch.from_numpy(x).to(dev) for x in (m.vertices, m.indices, cfg["origins"]))
+    out = torch.empty((m.n_vertices, 64, 64), dtype=torch.int16, device=dev)
+    ts = []
+    for it in range(reps + 1):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        mesh = rici.rici_create_mesh(v, t)
+        rici.rici_generate(mesh, o, cfg["R"], cfg["N"], out=out)
+        b.record(stream)
+        mesh.destroy()
+        torch.cuda.synchronize()
+        if it:
+            ts.append(a.elapsed_time(b))
+    ms = float(np.mean(ts))
+    del out
+    return {"workload": "C3: 10 bumpy tori 316x158 in a clutterbox of side 3, T=998,560, RICI at all 499,280 "
+                        "vertices", "ms": ms, "images_per_s": m.n_vertices / (ms / 1e3), "reps": reps}
+
+
+def extra_c2(rici, torch, dev, stream, flush, reps=5, simt=True):
+    """The round-1 C2 step (BASELINE configs[1]): mesh + RICI at all 34,848 vertices of the
+    264x132 torus + CRSS self-search (1.21e9 comparisons); and the SIMT CRSS path on it."""
+    import synth
+    cfg = synth.config_c2()
+    m = cfg["mesh"]
+    n = m.n_vertices
+    v, t, o = (torch.from_numpy(x).to(dev) for x in (m.vertices, m.indices, cfg["origins"]))
+    imgs = torch.empty((n, 64, 64), dtype=torch.int16, device=dev)
+    rk = torch.empty(n, dtype=torch.int32, device=dev)
+    ts = {"step": [], "gen": [], "crss": []}
+    for it in range(reps + 1):
+        flush.zero_()
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        e[0].record(stream)
+        mesh = rici.rici_create_mesh(v, t)
+        rici.rici_generate(mesh, o, cfg["R"], cfg["N"], out=imgs)
+        e[1].record(stream)
+        rici.rici_crss_search(imgs, imgs, out=rk)
+        e[2].record(stream)
+        mesh.destroy()
+        torch.cuda.synchronize()
+        if it:
+            ts["step"].append(e[0].elapsed_time(e[2]))
+            ts["gen"].append(e[0].elapsed_time(e[1]))
+            ts["crss"].append(e[1].elapsed_time(e[2]))
+    step = float(np.mean(ts["step"]))
+    res = {"workload": "C2: bumpy torus 264x132 (T=69,696), RICI at all 34,848 vertices, CRSS self-search "
+                       "34,848 x 34,848", "ms_per_step": step, "images_per_s": n / (step / 1e3),
+           "construction_ms": float(np.mean(ts["gen"])), "crss_ms": float(np.mean(ts["crss"])),
+           "comparisons_per_s": float(n) * n / (float(np.mean(ts["crss"])) / 1e3), "reps": reps}
+    if simt:
+        tt = []
+        for it in range(3):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            r_simt = rici.rici_crss_search(imgs, imgs, simt=True)
+            b.record(stream)
+            torch.cuda.synchronize()
+            if it:
+                tt.append(a.elapsed_time(b))
+        d = torch.diff(imgs.to(torch.int32) & 0xFFFF, dim=2)
+        terms = float(int((d != 0).sum())) * n
+        t_s = float(np.mean(tt)) / 1e3
+        pk = SMS * LANES_PER_SM * 1965.0 * 1e6
+        res["crss_simt_path"] = {
+            "ms": t_s * 1e3, "comparisons_per_s": float(n) * n / t_s,
+            "ranks_equal_tensor_path": bool(torch.equal(r_simt, rk)),
+            "roofline": {"bound": "alu", "achieved": terms * CRSS_OPS_PER_TERM / t_s / 1e12, "peak": pk / 1e12,
+                         "unit": "Tops/s", "frac": terms * CRSS_OPS_PER_TERM / t_s / pk,
+                         "algorithmic": f"{CRSS_OPS_PER_TERM} int ops per masked needle term"},
+            "note": "the north star's SIMT streaming compare (DESIGN.md 6.3), rici_crss_search(simt=True)"}
+    return res
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
 
     import paper_2007_02306_b200 as rici
     from paper_2007_02306_b200 import dist as rdist
+    import synth
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -229,41 +354,44 @@ def run_gpu(args):
         dist.init_process_group("nccl", device_id=dev)
     rici._lib.load()
 
-    cfg = workload(rank)
-    m = cfg["mesh"]
-    R, N = cfg["R"], cfg["N"]
-    n = m.n_vertices
-    v_d = torch.from_numpy(m.vertices).to(dev)
-    t_d = torch.from_numpy(m.indices).to(dev)
-    o_d = torch.from_numpy(cfg["origins"]).to(dev)
-    imgs = torch.empty((n, N, N), dtype=torch.int16, device=dev)
-    needles = torch.empty((workload(0)["mesh"].n_vertices if world > 1 else n, N, N), dtype=torch.int16, device=dev)
-    ranks_d = torch.empty(n, dtype=torch.int32, device=dev)
+    cfg = synth.config_c4() if rank == 0 else None
+    ref, sc = (cfg["reference"], cfg["scene"]) if rank == 0 else (None, None)
+    R, N = 0.3, 64
+    host = [ref.vertices, ref.indices, ref.origins, sc.vertices, sc.indices, sc.origins] if rank == 0 else [None] * 6
+    rv, rt, ro, sv, st, so = _bcast_mesh_arrays(host, dev, world, rank)
+    n_ref, n_sc = ro.shape[0], so.shape[0]
+    lo_r, hi_r = rdist.shard_range(n_ref, world, rank)
+    lo_h, hi_h = rdist.shard_range(n_sc, world, rank)
+    needles = torch.empty((n_ref, N, N), dtype=torch.int16, device=dev)
+    hay = torch.empty((hi_h - lo_h, N, N), dtype=torch.int16, device=dev)
+    ranks_d = torch.empty(n_ref, dtype=torch.int32, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > L2 (126 MB)
     stream = torch.cuda.current_stream()
+    ev = {k: [] for k in ("step", "needles", "hay", "crss")}
 
-    ev = {k: [] for k in ("step", "mesh", "gen", "crss")}
-
-    def step(record: bool):
+    def step(record: bool, src=None, out_ranks=None):
+        v = src or (rv, rt, ro, sv, st, so)
         e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
         e[0].record(stream)
-        mesh = rici.rici_create_mesh(v_d, t_d)
+        m_ref = rici.rici_create_mesh(v[0], v[1])
+        rdist.generate_sharded(m_ref, v[2], R, N, out=needles[lo_r:hi_r])
+        rdist.all_gather_images(needles, n_ref)
         e[1].record(stream)
-        rici.rici_generate(mesh, o_d, R, N, out=imgs)
+        m_sc = rici.rici_create_mesh(v[3], v[4])
+        rdist.generate_sharded(m_sc, v[5], R, N, out=hay)
         e[2].record(stream)
         if world == 1:
-            rici.rici_crss_search(imgs, imgs, out=ranks_d)
+            rici.rici_crss_search(needles, hay, out=ranks_d if out_ranks is None else out_ranks)
         else:
-            if rank == 0:
-                needles.copy_(imgs)
-            rdist.broadcast_images(needles, 0)
-            rdist.search_sharded(needles, imgs, rank * n, N)
+            r = rdist.search_sharded(needles, hay, lo_h, N)
+            (ranks_d if out_ranks is None else out_ranks).copy_(r.to(torch.int32))
         e[3].record(stream)
-        mesh.destroy()
+        m_ref.destroy()
+        m_sc.destroy()
         if record:
             ev["step"].append((e[0], e[3]))
-            ev["mesh"].append((e[0], e[1]))
-            ev["gen"].append((e[1], e[2]))
+            ev["needles"].append((e[0], e[1]))
+            ev["hay"].append((e[1], e[2]))
             ev["crss"].append((e[2], e[3]))
 
     for _ in range(max(args.warmup, 0)):
@@ -290,39 +418,25 @@ def run_gpu(args):
         wall = time.perf_counter() - t0
     launches = rici.rici_launch_count() - launches0
     rici.rici_set_kernel_timing(False)
-    gen_kernel_ms, n_gen_k = rici.rici_kernel_time_ms(0)       # generate_kernel, per launch
-    mma_kernel_ms, n_mma_k = rici.rici_kernel_time_ms(1)       # tcgen05 GEMM, per search call
+    gen_kernel_ms, n_gen_k = rici.rici_kernel_time_ms(0)       # generate_kernel, per call (2 per step)
+    mma_kernel_ms, n_mma_k = rici.rici_kernel_time_ms(1)       # tcgen05 GEMM launches, per search call
 
     def ms(k):
         return float(np.mean([a.elapsed_time(b) for a, b in ev[k]]))
 
-    step_ms, gen_ms, crss_ms, mesh_ms = ms("step"), ms("gen"), ms("crss"), ms("mesh")
-    step_ms_max = step_ms
+    step_ms, nd_ms, hay_ms, crss_ms = ms("step"), ms("needles"), ms("hay"), ms("crss")
+    local_step = step_ms
     if world > 1:
-        t = torch.tensor([step_ms, gen_ms, crss_ms, gen_kernel_ms, mma_kernel_ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([step_ms, nd_ms, hay_ms, crss_ms, mma_kernel_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        step_ms_max, gen_ms, crss_ms, gen_kernel_ms, mma_kernel_ms = [float(x) for x in t.cpu()]
+        step_ms, nd_ms, hay_ms, crss_ms, mma_kernel_ms = [float(x) for x in t.cpu()]
 
-    # ---- end-to-end through the public API with HOST buffers (every rank): mesh and origins
-    # from pinned host memory (H2D inside the library), ranks back to host memory (D2H)
-    vh = torch.from_numpy(m.vertices).pin_memory()
-    th = torch.from_numpy(m.indices).pin_memory()
-    oh = torch.from_numpy(cfg["origins"]).pin_memory()
-    rh = torch.empty(needles.shape[0] if world > 1 else n, dtype=torch.int32).pin_memory()
-
-    def e2e_step():
-        mesh = rici.rici_create_mesh(vh, th)                     # H2D inside the library
-        rici.rici_generate(mesh, oh, R, N, out=imgs)             # origins H2D inside
-        if world == 1:
-            rici.rici_crss_search(imgs, imgs, out=rh)            # ranks D2H + sync inside
-        else:
-            if rank == 0:
-                needles.copy_(imgs)
-            rdist.broadcast_images(needles, 0)
-            rh.copy_(rdist.search_sharded(needles, imgs, rank * n, N).to(torch.int32))   # D2H
-        mesh.destroy()
+    # ---- end-to-end through the public API with HOST buffers: meshes and oriented points from
+    # pinned host memory (H2D inside rici_create_mesh / rici_generate), ranks to pinned host memory
+    hv = [torch.from_numpy(x.cpu().numpy()).pin_memory() for x in (rv, rt, ro, sv, st, so)]
+    rh = torch.empty(n_ref, dtype=torch.int32).pin_memory()
     for _ in range(2):
-        e2e_step()
+        step(False, src=hv, out_ranks=rh)
         flush.zero_()
     torch.cuda.synchronize()
     tt = []
@@ -331,155 +445,121 @@ def run_gpu(args):
         if world > 1:
             dist.barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)                                          # device clock, like the step
-        e2e_step()
-        b.record(stream)                                          # after the ranks' D2H completed
+        a.record(stream)
+        step(False, src=hv, out_ranks=rh)
+        b.record(stream)
         torch.cuda.synchronize()
-        tt.append(a.elapsed_time(b) / 1e3)
+        tt.append(a.elapsed_time(b))
         flush.zero_()
-    e2e_ms = float(np.mean(tt)) * 1e3
+    e2e_ms = float(np.mean(tt))
     if world > 1:
         tmax = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
         e2e_ms = float(tmax.item())
-    e2e = {"value": n * world / (e2e_ms / 1e3), "unit": "images/s",
-           "h2d_bytes_per_step": int(vh.numel() * 4 + th.numel() * 4 + oh.numel() * 4),
+    h2d = int(sum(x.numel() * x.element_size() for x in (hv[0], hv[1], hv[3], hv[4]))
+              + (hi_r - lo_r + hi_h - lo_h) * 24)
+    e2e = {"value": (n_ref + n_sc) / (e2e_ms / 1e3), "unit": "images/s", "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": int(rh.numel() * 4), "ms_per_step": e2e_ms,
-           "note": "per rank; max over ranks" if world > 1 else "single GPU"}
+           "note": ("per rank, max over ranks; " if world > 1 else "") +
+                   "meshes + this rank's oriented points H2D inside the library calls, ranks D2H"}
+
+    ranks_ok = None
+    if world > 1:                              # ranks identical on every rank (all-reduced counts)
+        chk = ranks_d.to(torch.int64).sum().reshape(1)
+        allv = [torch.zeros_like(chk) for _ in range(world)]
+        dist.all_gather(allv, chk)
+        ranks_ok = all(int(x) == int(chk) for x in allv)
+    rank0_frac = float((ranks_d == 0).float().mean())
 
     if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
+        dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel: the tcgen05 int8 GEMM that ranks all pairs
-    # (DESIGN.md 6.2).  Algorithmic ops per comparison = 2 x K with K = 2 x 4096 int8 features;
-    # peak = the nominal dense int8 4.5 POPS (the measured-derived figures ride along).
     pk, src = peaks()
     sm_mhz = pk.get("sm_max_mhz", 1965.0)
-    imgs_np = imgs.cpu().numpy().view(np.uint16)
-    comparisons = float(imgs_np.shape[0]) * n                # per rank
-    n_total_hay = n * world
-    crss_s = crss_ms / 1e3
-    mma = os.environ.get("RICI_CRSS_PATH", "") != "simt"
-    sparse = mma and os.environ.get("RICI_MMA_MODE", "3") == "3"
-    if mma and n_mma_k > 0:
-        K = 2 * 4096
-        kern_s = mma_kernel_ms / 1e3                               # the GEMM launches, live events
-        achieved = comparisons * 2.0 * K / kern_s / 1e12          # logical int8 ops/s (Tops/s)
-        # measured bf16 x the guide's nominal ratio for this dtype (dense int8 2x, 2:4 int8 4x)
-        derived = (4.0 if sparse else 2.0) * pk.get("bf16_tflops", 1587.6)
-        arch = SMS * 8192 * 2 * sm_mhz * 1e6 / 1e12                # 8192 int8 MAC/clk/SM at sm_max
-        sp_rate = None
-        try:
-            with open(os.path.join(ROOT, "profiles", "int8_sparse_rate.json")) as f:
-                sp_rate = json.load(f)["sparse"]["logical_tops"]
-        except Exception:
-            pass
-        if sparse:   # 2:4-sparse needle operand: NVIDIA's doubled (sparse) figure is the ceiling
-            peak = 9000.0
-            kname = ("crss_mma_sp_kernel (tcgen05.mma.sp.cta_group::2.kind::i8, 2:4 needle rows, 4-CTA clusters "
-                     "with B multicast) + the dense subset pass on a side stream")
-        else:
-            peak = 4500.0                                          # nominal dense int8 (guide table)
-            kname = "crss_mma2_kernel (tcgen05.mma.cta_group::2.kind::i8, TMA, TMEM)"
-        traffic, tsrc = ncu_traffic("crss_mma_sp_kernel" if sparse else "crss_mma2_kernel")
-        roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": traffic,
-                "traffic_source": tsrc,
-                "kernel": kname,
-                "kernel_ms": mma_kernel_ms, "kernel_launches_timed": n_mma_k,
-                "timing": "CUDA events recorded by the library on the launch stream around each GEMM launch "
-                          "in the timed region (rici_set_kernel_timing / rici_kernel_time_ms)",
-                "frac_of_whole_search_call": comparisons * 2.0 * K / crss_s / 1e12 / peak,
-                "dtype": "int8 (2:4-sparse needle rows) x int8 -> int32" if sparse else "int8 x int8 -> int32",
-                "peak_source": ("nominal 2:4-sparse int8 9 POPS (2 x the dense 4.5 POPS of B200_PROFILING.md, whose "
-                                "doubled vendor figures are the 2:4 ones); the measured sparse issue rate is "
-                                "profiles/int8_sparse_rate.json" if sparse else
-                                "nominal dense int8 4.5 POPS (B200_PROFILING.md table)") +
-                               f".  The measured-derived figure (bf16 dense burst {pk.get('bf16_tflops', 1587.6)}"
-                               f" x {4 if sparse else 2} = {derived:.0f}) and cuBLAS int8 (profiles/int8_peak.json) "
-                               "are power-limited on random operands",
-                "frac_vs_measured_sparse_rate": (achieved / sp_rate) if (sparse and sp_rate) else None,
-                "dense_equivalent_frac_of_dense_peak": achieved / 4500.0,
-                "frac_vs_measured_derived": achieved / derived,
-                "frac_vs_arch_at_sm_max": achieved / arch,
-                "algorithmic": f"2 x {K} int8 MACs per comparison x {comparisons:.0f} comparisons"}
-        try:
-            with open(os.path.join(ROOT, "profiles", "int8_peak.json")) as f:
-                roof["int8_cublas_measured_tops"] = json.load(f)["int8_tops_burst"]
-        except Exception:
-            pass
-    else:
-        d = np.diff(imgs_np.astype(np.int32), axis=2)
-        nnz = int((d != 0).sum())
-        terms = float(nnz) * n
-        achieved = terms * CRSS_OPS_PER_TERM / crss_s / 1e12
-        peak = SMS * LANES_PER_SM * sm_mhz * 1e6 / 1e12
-        traffic, tsrc = ncu_traffic("crss_tile_kernel")
-        roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s",
-                "frac": achieved / peak, "traffic": traffic, "traffic_source": tsrc,
-                "kernel": "crss_tile_kernel (SIMT; timed as the rici_crss_search call)",
-                "peak_source": f"{SMS} SMs x {LANES_PER_SM} INT32 lanes x sm_max {sm_mhz} MHz ({src} clock)",
-                "algorithmic": f"{CRSS_OPS_PER_TERM} int ops per masked term; {nnz} masked needle terms "
-                               f"x {n} haystack images per rank"}
-    roof["hbm_equivalent_frac"] = comparisons * 8192 / crss_s / 1e9 / pk.get("hbm_gbs", 6548.8)
-    # the north star's own CRSS design (warp-cooperative integer streaming compare over the
-    # needle change lists, ballot/popc rank) on the same images, outside the step
-    simt_line = None
-    if world == 1 and mma and not args.no_cpu_baseline:
-        ts = []
-        for it in range(3):
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            flush.zero_()
-            a.record(stream)
-            r_simt = rici.rici_crss_search(imgs, imgs, simt=True)
-            b.record(stream)
-            torch.cuda.synchronize()
-            if it:
-                ts.append(a.elapsed_time(b))
-        d = np.diff(imgs_np.astype(np.int32), axis=2)
-        terms = float(int((d != 0).sum())) * n
-        t_s = float(np.mean(ts)) / 1e3
-        simt_line = {"ms": t_s * 1e3, "comparisons_per_s": comparisons / t_s,
-                     "ranks_equal_tensor_path": bool(torch.equal(r_simt.cpu(), ranks_d.cpu())),
-                     "roofline": {"bound": "alu", "achieved": terms * CRSS_OPS_PER_TERM / t_s / 1e12,
-                                  "peak": SMS * LANES_PER_SM * sm_mhz * 1e6 / 1e12, "unit": "Tops/s",
-                                  "frac": terms * CRSS_OPS_PER_TERM / t_s / (SMS * LANES_PER_SM * sm_mhz * 1e6),
-                                  "algorithmic": f"{CRSS_OPS_PER_TERM} int ops per masked needle term"},
-                     "note": "rici_crss_search(simt=True), whole call, not part of the timed step"}
-    images_per_s = n_total_hay / (step_ms_max / 1e3)
-    spp = segments_per_pair(cfg)
-    alu_peak = SMS * LANES_PER_SM * sm_mhz * 1e6 / 1e12
-    P_pairs = float(n) * m.n_triangles
-    W = 43.0 * P_pairs + 40.0 * spp * P_pairs + 3.0 * N * N * n
-    construction = {"ms": gen_ms, "kernel_ms": gen_kernel_ms, "images_per_s": n / (gen_ms / 1e3),
-                    "paper_literal_ops": W, "segments_per_pair": spp,
-                    "paper_literal_frac": W / (gen_ms / 1e3) / (alu_peak * 1e12),
-                    "note": "W = 43 P + 40 S + 3 N^2 n (brute-force pairs); the exact cull skips "
-                            "provably-zero pairs, so this fraction can exceed 1"}
+    comparisons = float(n_ref) * n_sc
+    cmp_rank = float(n_ref) * (hi_h - lo_h)
+    # ---- roofline of the CRSS GEMM: algorithmic ops = 2 x K int8 per comparison;
+    # peak = measured bf16 burst x the guide's nominal ratio for 2:4-sparse int8 (x2 int8, x2 2:4)
+    achieved = cmp_rank * 2.0 * K_FEAT / (mma_kernel_ms / 1e3) / 1e12 if n_mma_k else None
+    peak = 4.0 * pk.get("bf16_tflops", 1590.0)
+    sp_rate = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "int8_sparse_rate.json")) as f:
+            sp_rate = json.load(f)["sparse"]["logical_tops"]
+    except Exception:
+        pass
+    traffic, tsrc = ncu_traffic("crss_mma_sp_kernel")
+    roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": achieved / peak if achieved else None, "traffic": traffic, "traffic_source": tsrc,
+            "kernel": "crss_mma_sp_kernel (tcgen05.mma.sp.cta_group::2.kind::i8, 2:4 needle rows, 4-CTA clusters "
+                      "with B multicast) + the dense subset and side slice on a side stream",
+            "kernel_ms": mma_kernel_ms, "kernel_launches_timed": n_mma_k,
+            "timing": "CUDA events recorded by the library on the launch stream around each search call's GEMM "
+                      "launches in the timed region (rici_set_kernel_timing / rici_kernel_time_ms)",
+            "peak_source": (f"{src} bf16 dense burst {pk.get('bf16_tflops')} TFLOP/s x 4 (int8 = 2x bf16, 2:4 "
+                            f"sparsity = 2x dense: the B200_PROFILING.md nominal ratios)"),
+            "frac_vs_sustained_derived": (achieved / (4.0 * pk["bf16_tflops_sustained"])
+                                          if achieved and pk.get("bf16_tflops_sustained") else None),
+            "frac_vs_nominal_9pops": achieved / 9000.0 if achieved else None,
+            "frac_vs_probed_sparse_rate": (achieved / sp_rate) if (achieved and sp_rate) else None,
+            "frac_of_whole_search_call": cmp_rank * 2.0 * K_FEAT / (crss_ms / 1e3) / 1e12 / peak,
+            "dtype": "int8 (2:4-sparse needle rows) x int8 -> int32",
+            "algorithmic": f"2 x {K_FEAT} int8 MACs per comparison x {cmp_rank:.0f} comparisons per rank",
+            "hbm_equivalent_frac": cmp_rank * 8192 / (crss_ms / 1e3) / 1e9 / pk.get("hbm_gbs", 6548.8),
+            "hbm_equivalent_note": "comparisons/s x 8192 B (the north star's streaming bytes) / measured HBM: "
+                                   "the GEMM reuses each staged haystack row across 512 needles"}
+
+    cb = None
+    if world == 1 and not args.no_cpu_baseline:
+        h_host = hay.cpu().numpy().view(np.uint16)
+        n_host = needles.cpu().numpy().view(np.uint16)
+        cfg_h = cfg
+        cb = oracle_c4_sample(cfg_h, 64, 64, haystack=h_host, needles=n_host)
+        del h_host, n_host
+
+    alu_peak = SMS * LANES_PER_SM * sm_mhz * 1e6
+    T_sc, T_ref = sc.n_triangles, ref.n_triangles
+    P_pairs = float(n_sc) * T_sc + float(n_ref) * T_ref
+    construction = {"ms": nd_ms + hay_ms, "needles_ms": nd_ms, "haystack_ms": hay_ms,
+                    "images_per_s": (n_ref + n_sc) / ((nd_ms + hay_ms) / 1e3),
+                    "haystack_images_per_s": n_sc / (hay_ms / 1e3),
+                    "generate_kernel_ms_mean_per_call": gen_kernel_ms, "generate_calls_timed": n_gen_k,
+                    "note": "events around mesh staging + generate (+ the needles' all-gather at N>1)"}
+    if cb is not None:
+        W = (43.0 * P_pairs + 40.0 * (cb["segments_per_pair"] * n_sc * T_sc + cb["segments_per_pair_ref"] * n_ref * T_ref)
+             + 3.0 * N * N * (n_sc + n_ref))
+        construction.update({"paper_literal_ops": W, "segments_per_pair": cb["segments_per_pair"],
+                             "paper_literal_frac": W / ((nd_ms + hay_ms) / 1e3) / alu_peak,
+                             "paper_literal_note": "W = 43 P + 40 S + 3 N^2 n over brute-force pairs P (P:123); "
+                                                   "the exact cull skips provably-zero pairs, so this can exceed 1"})
     issue, isrc = ncu_metric("generate_kernel", "smsp__issue_active.avg.pct_of_peak_sustained_active")
     if issue is not None:
         construction["issue_slot_utilisation"] = issue / 100.0
         construction["issue_source"] = isrc + " (ncu --set full; the kernel is issue-bound)"
-    cb = cpu_baseline(cfg) if world == 1 and not args.no_cpu_baseline else None
-    line = {"metric": METRIC, "value": images_per_s, "unit": "images/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms_max,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32/i8",
+
+    extras = {}
+    if world == 1 and not args.no_extras:
+        del hay
+        torch.cuda.empty_cache()
+        extras["c3_construction"] = extra_c3(rici, torch, dev, stream, flush)
+        extras["c2_step"] = extra_c2(rici, torch, dev, stream, flush)
+    images = n_ref + n_sc
+    line = {"metric": METRIC, "value": images / (step_ms / 1e3), "unit": "images/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32/i8",
             "data": "synthetic",
-            "config": {"workload": "C2: bumpy torus 264x132 (T=69,696), RICI 64x64 at all 34,848 "
-                                   "vertices, R=0.3, CRSS self-search 34,848 x 34,848"
-                                   + ("" if world == 1 else f"; weak: {world} objects, haystack sharded"),
-                       "images_per_rank": n, "comparisons_per_step": comparisons * world,
-                       "l2": "flushed between timed steps (256 MB write); haystack 285 MB > L2",
-                       "parallelism": f"dp{world}"},
-            "comparisons_per_s": comparisons * world / (step_ms_max / 1e3),
+            "config": {"workload": WORKLOAD, "images_per_step": images, "comparisons_per_step": comparisons,
+                       "l2": "inputs > L2 (haystack 8.2 GB) and a 256 MB L2 flush between timed steps",
+                       "parallelism": f"dp{world}: scene and reference vertices sharded, haystack sharded, "
+                                      "needles all-gathered" if world > 1 else "single GPU"},
+            "comparisons_per_s": comparisons / (step_ms / 1e3),
             "construction": construction,
-            "crss": {"ms": crss_ms, "comparisons_per_s": comparisons / crss_s},
-            "mesh_staging_ms": mesh_ms,
-            "crss_simt_path": simt_line,
+            "crss": {"ms": crss_ms, "comparisons_per_s": comparisons / (crss_ms / 1e3), "mode": "full",
+                     "rank0_fraction": rank0_frac, "ranks_identical_on_all_ranks": ranks_ok},
             "roofline": roof, "cpu_baseline": cb, "e2e": e2e, "gpu_launches": int(launches),
-            "clocks": clk.summary(), "bench_wall_s": wall}
+            "clocks": clk.summary(), "bench_wall_s": wall, "rank0_local_step_ms": local_step}
+    line.update(extras)
     print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
@@ -492,6 +572,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="rici", choices=["rici", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the C3 / C2 extra keys")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

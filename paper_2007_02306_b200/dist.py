@@ -42,35 +42,66 @@ def cuda_ops() -> SearchOps:
     return SearchOps(pairs=rici_crss_pairs, count_below=rici_crss_count_below)
 
 
+def _world_rank(group=None) -> tuple[int, int]:
+    if not dist.is_initialized():
+        return 1, 0
+    return dist.get_world_size(group), dist.get_rank(group)
+
+
 def generate_sharded(mesh, origins: torch.Tensor, support_radius: float, n_bins: int = 64,
-                     group=None, generate: Callable | None = None):
-    """Each rank generates the images of its block of ``origins`` (the full [n,6] array).
+                     group=None, generate: Callable | None = None, out: torch.Tensor | None = None):
+    """Each rank generates the images of its block of ``origins`` (the full [n,6] array; the
+    mesh is replicated, no collective).  ``out`` (optional) receives the block: [hi-lo, N, N].
     Returns (images of the block, (lo, hi))."""
-    world = dist.get_world_size(group) if dist.is_initialized() else 1
-    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    world, rank = _world_rank(group)
     lo, hi = shard_range(origins.shape[0], world, rank)
     if generate is None:
         from . import rici_generate as generate
+    if out is not None:
+        return generate(mesh, origins[lo:hi].contiguous(), support_radius, n_bins, out=out), (lo, hi)
     return generate(mesh, origins[lo:hi].contiguous(), support_radius, n_bins), (lo, hi)
 
 
+def all_gather_images(images: torch.Tensor, n_total: int, group=None) -> torch.Tensor:
+    """In place: ``images`` [n_total, N, N] holds this rank's block shard_range(n_total, ...)
+    on entry and every rank's block on exit (the needles generated sharded).
+    Blocks differ in size by at most one image, so each is sent padded to the largest as raw
+    bytes (no int16 type in NCCL/gloo) with one all_gather_into_tensor."""
+    world, rank = _world_rank(group)
+    if world == 1:
+        return images
+    per = -(-n_total // world)
+    img_bytes = images[0].numel() * images.element_size() if n_total else 0
+    lo, hi = shard_range(n_total, world, rank)
+    send = torch.zeros(per * img_bytes, dtype=torch.uint8, device=images.device)
+    send[: (hi - lo) * img_bytes] = images[lo:hi].reshape(-1).view(torch.uint8)
+    recv = torch.empty(world * per * img_bytes, dtype=torch.uint8, device=images.device)
+    dist.all_gather_into_tensor(recv, send, group=group)
+    flat = images.reshape(-1).view(torch.uint8)
+    for r in range(world):
+        a, b = shard_range(n_total, world, r)
+        if r != rank and b > a:
+            flat[a * img_bytes: b * img_bytes] = recv[r * per * img_bytes: (r * per + b - a) * img_bytes]
+    return images
+
+
 def broadcast_images(images: torch.Tensor, src: int = 0, group=None) -> torch.Tensor:
-    """Broadcast ``images`` (uint16 counts in int16 storage, in place) from ``src``.  When every
-    count fits a byte -- RICI counts of one object rarely exceed a few tens -- the payload goes
-    as uint8, half the bytes; otherwise the raw bytes (neither NCCL nor gloo has an int16
-    type).  Exact either way."""
+    """Broadcast ``images`` (uint16 counts in int16 storage, in place) from global rank ``src``
+    (the torch.distributed convention for ``dist.broadcast``).  When every count fits a byte --
+    RICI counts of one object rarely exceed a few tens -- the payload goes as uint8, half the
+    bytes; otherwise the raw bytes (neither NCCL nor gloo has an int16 type).  Exact either way."""
     dev = images.device
+    me = dist.get_rank() == src
     small = torch.zeros(1, dtype=torch.int32, device=dev)
-    if dist.get_rank(group) == src and images.numel():
+    if me and images.numel():
         small.fill_(int(images.view(torch.int16).to(torch.int32).bitwise_and(0xFFFF).max().item() <= 255))
     dist.broadcast(small, src, group=group)
     if not int(small.item()):
         dist.broadcast(images.view(torch.uint8), src, group=group)   # NCCL/gloo have no int16: bytes
         return images
-    packed = images.to(torch.uint8) if dist.get_rank(group) == src else torch.empty(images.shape, dtype=torch.uint8,
-                                                                                     device=dev)
+    packed = images.to(torch.uint8) if me else torch.empty(images.shape, dtype=torch.uint8, device=dev)
     dist.broadcast(packed, src, group=group)
-    if dist.get_rank(group) != src:
+    if not me:
         images.copy_(packed.to(torch.int16))
     return images
 

@@ -114,8 +114,15 @@ def test_scene_cuda_against_oracle(oracle_mod):
         m = rici.rici_create_mesh(torch.from_numpy(mesh.vertices).cuda(), torch.from_numpy(mesh.indices).cuda())
         f = rici.rici_clutter_fraction(m, torch.from_numpy(tag).cuda(), torch.from_numpy(origins).cuda(), R)
         m.destroy()
-        want = oracle_mod.clutter_fraction(mesh.vertices, mesh.indices, tag, origins, R)[0]
-        assert np.abs(f.cpu().numpy().astype(np.float64) - want).max() <= 2e-4
+        # G17's inside test is a float decision at the cylinder wall, like a RICI bin edge: a
+        # sub-triangle centroid within tau = 1e-5 R of the wall may go either way.  The GPU value
+        # must lie in the oracle's bracket over R(1 - 1e-5), R, R(1 + 1e-5) (+1e-5 for float
+        # accumulation) -- the same attribution width as the RICI parity rule
+        w = [oracle_mod.clutter_fraction(mesh.vertices, mesh.indices, tag, origins, R * (1 + k * 1e-5))[0]
+             for k in (-1, 0, 1)]
+        lo, hi = np.minimum.reduce(w) - 1e-5, np.maximum.reduce(w) + 1e-5
+        g = f.cpu().numpy().astype(np.float64)
+        assert ((g >= lo) & (g <= hi)).all(), float(np.max(np.maximum(lo - g, g - hi)))
         return f.cpu().numpy()
 
     levels = [1, 3, 6]

@@ -13,7 +13,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2007_02306_b200.dist import SearchOps, broadcast_images, generate_sharded, search_sharded, shard_range
+from paper_2007_02306_b200.dist import (SearchOps, all_gather_images, broadcast_images, generate_sharded,
+                                        search_sharded, shard_range)
 
 
 def test_shard_range_partitions():
@@ -66,6 +67,12 @@ def _worker(rank, world, port, needles, haystack, origins, q):
         imgs, (lo, hi) = generate_sharded(None, torch.from_numpy(origins), 0.3, 64, generate=gen)
         gathered = [None] * world
         dist.all_gather_object(gathered, (lo, hi, imgs.numpy()))
+        # the same blocks generated into a full-size buffer and all-gathered in place (the
+        # bench's needle path); blocks of unequal size (n % world != 0) are padded on the wire
+        full_buf = torch.full((origins.shape[0], 64, 64), -7, dtype=torch.int16)
+        generate_sharded(None, torch.from_numpy(origins), 0.3, 64,
+                         generate=lambda mesh, o, R, N, out: out.copy_(gen(mesh, o, R, N)), out=full_buf[lo:hi])
+        all_gather_images(full_buf, origins.shape[0])
         # search: haystack split in contiguous blocks
         nh = haystack.shape[0]
         slo, shi = shard_range(nh, world, rank)
@@ -79,7 +86,7 @@ def _worker(rank, world, port, needles, haystack, origins, q):
         broadcast_images(big, 0)
         bcast_ok = bool(torch.equal(nd, torch.from_numpy(needles.view(np.int16)))) and int(big[0, 0, 5]) == -2
         ranks = search_sharded(nd, shard, slo, 64, ops=_oracle_ops())
-        q.put((rank, ranks.numpy(), gathered if rank == 0 else None, bcast_ok))
+        q.put((rank, ranks.numpy(), gathered if rank == 0 else None, bcast_ok, full_buf.numpy()))
     finally:
         dist.destroy_process_group()
 
@@ -105,8 +112,9 @@ def test_sharded_search_and_generate_equal_single_process(oracle_mod, world):
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    for rank, ranks, gathered, bcast_ok in res:
+    for rank, ranks, gathered, bcast_ok, full_buf in res:
         assert bcast_ok, rank
+        assert np.array_equal(full_buf.view(np.uint16), full), rank         # all_gather_images
         assert np.array_equal(ranks.astype(np.uint32), want), rank
         if gathered is not None:
             parts = sorted(gathered, key=lambda g: g[0])

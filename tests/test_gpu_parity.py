@@ -148,11 +148,15 @@ def test_adversarial(rici, oracle_mod, case):
         # every differing pixel must be an EXACT tie: flagged by the same stencil at
         # tau = 1e-12 R, far below float32 resolution (~6e-8 R), i.e. a decision whose double-
         # precision margin is zero up to rounding -- where FP32 and FP64 may both be right (G16)
+        # Exact ties are not errors (G16: both counts are correct); every OTHER differing pixel
+        # is a float32-vs-double rounding disagreement and counts against the north star's 1e-4
+        # budget, like on the workload meshes.
         tie = oracle_mod.rici_generate(m.vertices, m.indices, o, R, 64, fragile=True, tau_rel=1e-12)["fragile"]
         diff = g != ref["images"]
-        assert not (diff & ~tie).any(), f"{int((diff & ~tie).sum())} of {n_diff} differing pixels are not exact ties"
-        print(f"grid_soup: {n_diff} differing pixels, {int(tie.sum())} exact-tie pixels, "
-              f"{int(ref['fragile'].sum())} fragile of {diff.size}")
+        n_near = int((diff & ~tie).sum())
+        print(f"grid_soup: {n_diff} differing pixels ({n_near} not exact ties), {int(tie.sum())} exact-tie "
+              f"pixels, {int(ref['fragile'].sum())} fragile, of {diff.size}")
+        assert n_near <= 1e-4 * diff.size, f"{n_near} differing pixels that are not exact ties"
         assert n_diff <= 0.1 * ref["fragile"].sum()
     else:
         _assert_parity(g, ref)
