@@ -98,56 +98,70 @@ __device__ __forceinline__ void red_shared(unsigned addr, int v) {
 // (relative error ~1e-7) move decisions by far less than the 1e-5*R attribution bound.
 // `acc` is the image's [N][N+1] difference array as a shared-window address: column N is a
 // sink, so a range end at N needs no test, and coinciding ends cancel in place.
+//
+// Per layer the slice endpoints are affine in the row centre rc = r + 1/2 (beta = rc*delta -
+// R/2): E0 = a + t (c - a) on the long edge, t = (beta - z_a)/(z_c - z_a), and E1 on the
+// polyline a -> b -> c, E1 = a + u1 (b - a) + u2 (c - b) with u1 = (beta - z_a)/(z_b - z_a) and
+// u2 = (beta - z_b)/(z_c - z_b), every parameter saturated to [0, 1]: below the middle vertex
+// u2 = 0 and E1 lies on (a,b); above it u1 = 1 and E1 lies on (b,c) (step 1) -- no
+// branch per layer.  The saturation also makes a row the ceil-based range admits by rounding
+// (beta within ~1 ulp outside [z_a, z_c), G5) a zero-length slice (E0 = E1 = a or c), which
+// contributes nothing; t = rc*S + O is (beta - z_a)/(z_c - z_a) rearranged (a beta shift of a
+// few ulps, far inside tau).  The (x, y) pairs run as packed FP32x2 instructions (FFMA2/FADD2).
+__device__ __forceinline__ float2 f2(float x, float y) { return make_float2(x, y); }
+__device__ __forceinline__ float fma_sat(float a, float b, float c) {   // FFMA.SAT: clamp to [0, 1]
+    float r;
+    asm("fma.rn.ftz.sat.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+
 __device__ __forceinline__ void rasterise_triangle(unsigned acc, const Geometry &g,
                                                    float ax, float ay, float az, float bx,
                                                    float by, float bz, float cx, float cy,
                                                    float cz) {
     const int N = g.n;
-    int r_lo = first_at_or_above(az, g.inv_delta, g.row_off, N);
-    int r_hi = first_at_or_above(cz, g.inv_delta, g.row_off, N);
+    const int r_lo = first_at_or_above(az, g.inv_delta, g.row_off, N);
+    const int r_hi = first_at_or_above(cz, g.inv_delta, g.row_off, N);
     if (r_lo >= r_hi) { RICI_STAT(8, 1); return; }
 #if RICI_GEN_STATS
     bool stat_emitted = false;
 #endif
     RICI_STAT(4, r_hi - r_lo);
-    const float inv_ac = fast_rcp(cz - az);              // > 0 whenever a layer is inside
-    const float inv_ab = bz > az ? fast_rcp(bz - az) : 0.f;
-    const float inv_bc = cz > bz ? fast_rcp(cz - bz) : 0.f;
+    const float nh = -g.half_r;
+    const float i_ac = fast_rcp(cz - az);                // z_c > z_a whenever a layer is inside
+    const float st = g.delta * i_ac, ot = (nh - az) * i_ac;
+    float s1 = 0.f, o1 = 1.f, s2 = 0.f, o2 = 0.f;        // flat (a,b): E1 starts at b; flat (b,c): stays on (a,b)
+    if (bz > az) { const float i = fast_rcp(bz - az); s1 = g.delta * i; o1 = (nh - az) * i; }
+    if (cz > bz) { const float i = fast_rcp(cz - bz); s2 = g.delta * i; o2 = (nh - bz) * i; }
+    const float2 A = f2(ax, ay), AC = f2(cx - ax, cy - ay), AB = f2(bx - ax, by - ay), BC = f2(cx - bx, cy - by);
+    const float2 cm = f2(g.inv_delta, g.inv_delta), ch = f2(-0.5f, -0.5f);
     unsigned row = acc + 4u * (unsigned)(r_lo * (N + 1));
     const unsigned row_step = 4u * (unsigned)(N + 1);
     float rc = (float)r_lo + 0.5f;                        // r + 1/2, exact in float
     for (int r = r_lo; r < r_hi; ++r, row += row_step, rc += 1.f) {
-        float beta = fmaf(rc, g.delta, -g.half_r);
-        if (!(az <= beta && beta < cz)) continue;        // layer membership, half-open (G5)
         // Step 1: E0 on the long edge (a,c), E1 on (a,b) below / (b,c) above the middle vertex.
-        float t = (beta - az) * inv_ac;
-        float e0x = fmaf(t, cx - ax, ax), e0y = fmaf(t, cy - ay, ay);
-        float e1x, e1y;
-        if (beta < bz) {
-            float u = (beta - az) * inv_ab;
-            e1x = fmaf(u, bx - ax, ax); e1y = fmaf(u, by - ay, ay);
-        } else {
-            float u = (beta - bz) * inv_bc;
-            e1x = fmaf(u, cx - bx, bx); e1y = fmaf(u, cy - by, by);
-        }
+        const float t = fma_sat(rc, st, ot);
+        const float u1 = fma_sat(rc, s1, o1), u2 = fma_sat(rc, s2, o2);
+        const float2 e0 = __ffma2_rn(f2(t, t), AC, A);
+        const float2 e1 = __ffma2_rn(f2(u2, u2), BC, __ffma2_rn(f2(u1, u1), AB, A));
         // Step 2: rotate so E0E1 is parallel to x with the normalised direction D/|D| as
         // (cos, sin): the rotated x of E0 / E1 is (D.E0)/|D| / (D.E1)/|D|, so their signs are
         // those of D.E0 and D.E0 + |D|^2 -- the normalisation is only needed for |C| below.
-        const float dx = e1x - e0x, dy = e1y - e0y;
-        const float l2 = dx * dx + dy * dy;
-        if (l2 == 0.f) continue;                          // zero-length slice (G5)
-        const float de0 = fmaf(dx, e0x, dy * e0y);        // |D| * x0
+        const float2 d = __ffma2_rn(e0, f2(-1.f, -1.f), e1);
+        const float l2 = fmaf(d.x, d.x, d.y * d.y);
+        const float de0 = fmaf(d.x, e0.x, d.y * e0.y);    // |D| * x0
         // Steps 3-4: distances of E0, E1 from the axis; single range [min, max).
-        float r0 = fast_sqrt(e0x * e0x + e0y * e0y), r1 = fast_sqrt(e1x * e1x + e1y * e1y);
-        const int c_min = first_col_at_or_above(fminf(r0, r1), g.inv_delta, N);
-        const int c_max = first_col_at_or_above(fmaxf(r0, r1), g.inv_delta, N);
+        const float r0 = fast_sqrt(fmaf(e0.x, e0.x, e0.y * e0.y)), r1 = fast_sqrt(fmaf(e1.x, e1.x, e1.y * e1.y));
+        const float2 cf = __ffma2_rn(f2(fminf(r0, r1), fmaxf(r0, r1)), cm, ch);   // v/delta - 1/2
+        const int c_min = min(__float2int_ru(cf.x), N), c_max = min(__float2int_ru(cf.y), N);
         // Steps 5-6: double range [|C|, min) iff the x signs differ (x = 0 non-negative);
         // |C| = |rotated y| = |D x E0| / |D|.  Single: +1 at c_min, -1 at c_max.  Double:
-        // +2 at c_c, -1 at c_min, -1 at c_max.  Empty ranges cancel at one address.
+        // +2 at c_c, -1 at c_min, -1 at c_max.  Empty ranges (also a zero-length slice, whose
+        // r0 = r1 and de0 = 0) cancel at one address.
         const bool dbl = de0 < 0.f && de0 + l2 >= 0.f;
         int c_lo = c_min;
         if (dbl) {
-            const float y = fmaf(dx, e0y, -dy * e0x) * rsqrtf(l2);
+            const float y = fmaf(d.x, e0.y, -d.y * e0.x) * rsqrtf(l2);
             c_lo = min(first_col_at_or_above(fabsf(y), g.inv_delta, N), c_min);
         }
         if (c_lo == c_max) continue;                      // nothing in [c_lo, c_max)
