@@ -71,8 +71,11 @@ typedef enum {
  *   out_mesh   receives the handle (unchanged on error)
  * n_triangles = 0 is a valid empty scene (every image is zero); at most 268,435,456
  * triangles (RICI_ERR_INVALID_ARGUMENT beyond).
- * Index validation reads the indices, so this call synchronises `stream`;
- * an out-of-range index returns RICI_ERR_INVALID_ARGUMENT.                   */
+ * Index validation reads the indices, so this call synchronises `stream` once (after the
+ * validating first pass); an out-of-range index returns RICI_ERR_INVALID_ARGUMENT.  The
+ * spatial sort and chunk staging that follow run asynchronously on `stream`: a use of the mesh
+ * on another stream first waits for them (an event recorded by this call), and
+ * rici_destroy_mesh waits for them too.                                       */
 RICI_API rici_status rici_create_mesh(const float *vertices, int64_t n_vertices,
                              const int32_t *indices, int64_t n_triangles,
                              rici_stream_t stream, rici_mesh *out_mesh);
@@ -112,10 +115,13 @@ RICI_API rici_status rici_generate(rici_mesh mesh, const float *origins, int64_t
  *   out_ranks  [n_needles] uint32
  * Exact integer arithmetic (bit-exact for every input).
  * Kernels: for n_bins = 64 the counts run on the tensor cores (tcgen05 int8 GEMM of the
- * expanded Eq. 7, exact under a per-image guard |D_n| <= 63, |D_h| <= 15) and the few images
- * outside the guard are recounted by the SIMT kernel; this sizing step synchronises `stream`
- * once.  Other n_bins, or RICI_CRSS_PATH=simt in the environment, use the SIMT kernel only
- * (no synchronisation).  rici_crss_count_below follows the same rule.                    */
+ * expanded Eq. 7, exact under a per-image guard |D_n| <= 63, |D_h| <= 15) and the pairs with an
+ * image outside the guard are counted exactly by fallback kernels sized on the device (see
+ * rici_crss_guard_stats).  Other n_bins, or RICI_CRSS_PATH=simt in the environment, use the SIMT
+ * kernel only.  No path synchronises the host (device buffers; the calls can be captured in a
+ * CUDA graph).  Temporary workspace is stream-ordered (cudaMallocAsync) and, at n_bins = 64,
+ * about 2 x 8 KB per needle row plus 8 KB per haystack row.  rici_crss_count_below follows the
+ * same rules.                                                                             */
 RICI_API rici_status rici_crss_search(const uint16_t *needles, int64_t n_needles,
                              const uint16_t *haystack, int64_t n_haystack,
                              int32_t n_bins, uint32_t *out_ranks, rici_stream_t stream);
@@ -139,8 +145,11 @@ RICI_API rici_status rici_crss_search_ex(const uint16_t *needles, int64_t n_need
                                          int32_t n_bins, uint32_t flags, uint32_t *out_ranks,
                                          rici_stream_t stream);
 
-/* Sharding primitives (used by the multi-GPU layer).
- * rici_crss_pairs: out[k] = CRSS(needles[pairs[k][0]], haystack[pairs[k][1]]).
+/* Sharding primitives (used by the multi-GPU layer, SURVEY 8(e)).
+ * rici_crss_pairs: out[k] = CRSS(needles[pairs[k][0]], haystack[pairs[k][1]]) -- Eq. 7
+ *   (Listing 1) for an explicit pair list: the threshold pass a10, t_i =
+ *   CRSS(n_i, h_{k_i}) ("this threshold can be trivially precomputed"; G11 for k_i), run
+ *   by the rank that owns h_{k_i}.
  *   pairs [m][2] int64 (needle index, haystack index).  With HOST pairs every
  *   index is validated (RICI_ERR_INVALID_ARGUMENT); with DEVICE pairs an
  *   out-of-range pair yields out[k] = UINT64_MAX.                           */
@@ -150,13 +159,16 @@ RICI_API rici_status rici_crss_pairs(const uint16_t *needles, int64_t n_needles,
                             rici_stream_t stream);
 
 /* out_counts[i] = #{ j in [0,n_haystack) : CRSS(needles[i], haystack[j]) < thresholds[i] }
- * (overwritten, not accumulated).  thresholds [n_needles] uint64.            */
+ * (overwritten, not accumulated).  thresholds [n_needles] uint64.  With t_i = CRSS(n_i, h_i)
+ * this is the rank of P:388 ("lower ranks are better") with the best-tie rule of P:459 (strict
+ * <, G10) restricted to one haystack shard; the per-shard counts of all ranks sum to the rank. */
 RICI_API rici_status rici_crss_count_below(const uint16_t *needles, int64_t n_needles,
                                   const uint16_t *haystack, int64_t n_haystack, int32_t n_bins,
                                   const uint64_t *thresholds, uint32_t *out_counts,
                                   rici_stream_t stream);
 
-/* Full distance matrix out[i][j] = CRSS(needles[i], haystack[j]), uint64. */
+/* Full distance matrix out[i][j] = CRSS(needles[i], haystack[j]), uint64: Eq. 7,
+ * exact, asymmetric in its arguments (only the needle's changes are masked). SIMT kernel. */
 RICI_API rici_status rici_crss_distances(const uint16_t *needles, int64_t n_needles,
                                 const uint16_t *haystack, int64_t n_haystack, int32_t n_bins,
                                 uint64_t *out, rici_stream_t stream);
@@ -200,6 +212,16 @@ RICI_API uint64_t rici_launch_count(void);
 #define RICI_KERNEL_CRSS_MMA 1
 RICI_API rici_status rici_set_kernel_timing(int32_t enable);
 RICI_API rici_status rici_kernel_time_ms(int32_t kernel, float *out_mean_ms, int64_t *out_launches);
+
+/* Guard coverage of the tensor-core CRSS path (n_bins = 64) on the current device, accumulated
+ * over every count / search call since the last reset:
+ *   out[0] needles                       out[1] needles outside the int8 guard (|D_n| > 63)
+ *   out[2] haystack images               out[3] haystack images outside it (|D_h| > 15)
+ *   out[4] guard-valid needles that are not 2:4-sparse (the dense tensor pass)
+ * Pairs with an image outside the guard are counted exactly by the fallback kernels; these
+ * counters say how much work took that path.  Synchronises the device.  reset != 0 zeroes the
+ * counters after reading.  Errors: RICI_ERR_INVALID_ARGUMENT for a NULL out.                */
+RICI_API rici_status rici_crss_guard_stats(int64_t out[5], int32_t reset);
 
 /* "rici-b200 <version> sm_100a" */
 RICI_API const char *rici_version(void);

@@ -20,7 +20,8 @@ from ._lib import RiciError, check, load
 
 __all__ = ["Mesh", "RiciError", "rici_create_mesh", "rici_destroy_mesh", "rici_generate",
            "rici_crss_search", "rici_crss_search_ex", "rici_clutter_fraction", "rici_crss_pairs", "rici_crss_count_below", "rici_crss_distances",
-           "rici_launch_count", "rici_set_kernel_timing", "rici_kernel_time_ms", "rici_version",
+           "rici_launch_count", "rici_set_kernel_timing", "rici_kernel_time_ms", "rici_crss_guard_stats",
+           "rici_version",
            "library_path"]
 
 
@@ -241,3 +242,11 @@ def rici_kernel_time_ms(kernel: int) -> tuple[float, int]:
 
 def rici_version() -> str:
     return load().rici_version().decode()
+
+
+def rici_crss_guard_stats(reset: bool = False) -> dict:
+    """Guard coverage of the tensor-core CRSS path on the current device (include/rici.h)."""
+    out = (ctypes.c_int64 * 5)()
+    check(load().rici_crss_guard_stats(out, int(bool(reset))))
+    keys = ("needles", "needles_outside_guard", "haystack", "haystack_outside_guard", "needles_not_2_4")
+    return dict(zip(keys, (int(x) for x in out)))

@@ -15,7 +15,7 @@ LIB_PATH = os.path.join(_HERE, "librici.so")
 SYMBOLS = ["rici_create_mesh", "rici_destroy_mesh", "rici_mesh_num_triangles", "rici_generate",
            "rici_crss_search", "rici_crss_search_ex", "rici_crss_pairs", "rici_crss_count_below", "rici_crss_distances",
            "rici_clutter_fraction", "rici_last_error", "rici_launch_count", "rici_set_kernel_timing",
-           "rici_kernel_time_ms", "rici_version"]
+           "rici_kernel_time_ms", "rici_crss_guard_stats", "rici_version"]
 
 RICI_CRSS_SIMT = 1
 RICI_CRSS_EARLY_EXIT = 2
@@ -72,6 +72,8 @@ def load() -> ctypes.CDLL:
     lib.rici_set_kernel_timing.restype = st
     lib.rici_kernel_time_ms.argtypes = [i32, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(i64)]
     lib.rici_kernel_time_ms.restype = st
+    lib.rici_crss_guard_stats.argtypes = [ctypes.POINTER(i64), i32]
+    lib.rici_crss_guard_stats.restype = st
     lib.rici_version.argtypes = []
     lib.rici_version.restype = ctypes.c_char_p
     _lib = lib

@@ -17,6 +17,13 @@
 
 struct rici_mesh_s {
     rici::DeviceMesh m;
+    // staging (sort, kd refinement, chunk layout) finishes asynchronously on the creation stream:
+    // `ready` is recorded after it, and a use on another stream waits for it first
+    cudaStream_t created_on = nullptr;
+    cudaEvent_t ready = nullptr;
+    void wait_ready(cudaStream_t s) {
+        if (ready && s != created_on) cudaStreamWaitEvent(s, ready, 0);
+    }
     // one event per stream the mesh was read on, recorded after each use: rici_destroy_mesh
     // orders the frees after every recorded use, whatever the streams' flags
     std::mutex mu;
@@ -38,38 +45,44 @@ namespace rici {
 static std::atomic<unsigned long long> g_launches{0};
 void note_launches(int k) { g_launches.fetch_add((unsigned long long)k, std::memory_order_relaxed); }
 
-// ---- per-kernel timing: event pairs recorded around launches, drained by rici_kernel_time_ms
+// ---- per-kernel timing: event pairs recorded around one API call's launches of a timed kernel
+// (KernelTimer), drained by rici_kernel_time_ms.  The begin event travels with the caller's
+// timer, so calls on several threads / streams never mix their events.
 static std::atomic<int> g_timing{0};
 static std::mutex g_timing_mu;
 struct TimedLaunch { cudaEvent_t a, b; };
-static std::vector<TimedLaunch> g_timed[2];          // per kernel id: recorded pairs
+static std::vector<TimedLaunch> g_timed[2];          // per kernel id: recorded pairs (one per call)
 static std::vector<cudaEvent_t> g_event_pool;
-static cudaEvent_t g_open[2] = {nullptr, nullptr};  // begin event of the launch in flight
-static int64_t g_calls[2] = {0, 0};                  // API calls that recorded launches
 static cudaEvent_t take_event() {
     cudaEvent_t e = nullptr;
     if (!g_event_pool.empty()) { e = g_event_pool.back(); g_event_pool.pop_back(); }
-    else cudaEventCreate(&e);
+    else if (cudaEventCreate(&e) != cudaSuccess) { cudaGetLastError(); e = nullptr; }
     return e;
 }
-void timing_begin(int kernel, cudaStream_t s) {
-    if (!g_timing.load(std::memory_order_relaxed)) return;
+cudaEvent_t timing_begin(int kernel, cudaStream_t s) {
+    (void)kernel;
+    if (!g_timing.load(std::memory_order_relaxed)) return nullptr;
     std::lock_guard<std::mutex> lock(g_timing_mu);
     cudaEvent_t e = take_event();
-    if (e && cudaEventRecord(e, s) == cudaSuccess) g_open[kernel] = e;
+    if (e && cudaEventRecord(e, s) != cudaSuccess) { cudaGetLastError(); g_event_pool.push_back(e); e = nullptr; }
+    return e;
 }
-void timing_call(int kernel) {
-    if (!g_timing.load(std::memory_order_relaxed)) return;
+void timing_end(int kernel, cudaStream_t s, cudaEvent_t begin) {
+    if (!begin) return;
     std::lock_guard<std::mutex> lock(g_timing_mu);
-    ++g_calls[kernel];
-}
-void timing_end(int kernel, cudaStream_t s) {
-    if (!g_timing.load(std::memory_order_relaxed)) return;
-    std::lock_guard<std::mutex> lock(g_timing_mu);
-    if (!g_open[kernel]) return;
     cudaEvent_t e = take_event();
-    if (e && cudaEventRecord(e, s) == cudaSuccess) g_timed[kernel].push_back({g_open[kernel], e});
-    g_open[kernel] = nullptr;
+    if (e && cudaEventRecord(e, s) == cudaSuccess) {
+        g_timed[kernel].push_back({begin, e});
+    } else {
+        cudaGetLastError();
+        g_event_pool.push_back(begin);
+        if (e) g_event_pool.push_back(e);
+    }
+}
+void timing_release(cudaEvent_t begin) {
+    if (!begin) return;
+    std::lock_guard<std::mutex> lock(g_timing_mu);
+    g_event_pool.push_back(begin);
 }
 cudaError_t ensure_smem(const void *kernel, size_t bytes) {
     int dev = 0;
@@ -86,12 +99,19 @@ cudaError_t ensure_smem(const void *kernel, size_t bytes) {
     return e;
 }
 bool use_mma_path(int N) {
-    static int mode = -1;                  // 1 = tensor cores where applicable, 0 = SIMT only
-    if (mode < 0) {
+    static const int mode = [] {           // 1 = tensor cores where applicable, 0 = SIMT only
         const char *v = getenv("RICI_CRSS_PATH");
-        mode = (v && strcmp(v, "simt") == 0) ? 0 : 1;
-    }
+        return (v && strcmp(v, "simt") == 0) ? 0 : 1;
+    }();                                   // thread-safe initialisation (magic static)
     return mode == 1 && N == 64;
+}
+int env_int(const char *name, int dflt) {
+    const char *v = getenv(name);
+    return v ? atoi(v) : dflt;
+}
+double env_double(const char *name, double dflt) {
+    const char *v = getenv(name);
+    return v ? atof(v) : dflt;
 }
 }  // namespace rici
 
@@ -256,15 +276,24 @@ rici_status rici_kernel_time_ms(int32_t kernel, float *out_mean_ms, int64_t *out
         rici::g_event_pool.push_back(t.b);
     }
     rici::g_timed[kernel].clear();
-    const int64_t calls = rici::g_calls[kernel];
-    rici::g_calls[kernel] = 0;
-    *out_mean_ms = calls ? (float)(sum / (double)calls) : 0.f;
+    *out_mean_ms = cnt ? (float)(sum / (double)cnt) : 0.f;    // one pair per API call
     *out_launches = cnt;
     if (err != cudaSuccess) return cuda_fail(err, "rici_kernel_time_ms");
     return RICI_OK;
 }
 
-const char *rici_version(void) { return "rici-b200 0.1.0 sm_100a"; }
+rici_status rici_crss_guard_stats(int64_t out[5], int32_t reset) {
+    g_err.clear();
+    if (!out) return fail(RICI_ERR_INVALID_ARGUMENT, "null out");
+    if (rici_status st = check_device()) return st;
+    unsigned long long v[5] = {0, 0, 0, 0, 0};
+    cudaError_t e = rici::read_guard_stats(v, reset != 0);
+    if (e != cudaSuccess) return cuda_fail(e, "rici_crss_guard_stats");
+    for (int k = 0; k < 5; ++k) out[k] = (int64_t)v[k];
+    return RICI_OK;
+}
+
+const char *rici_version(void) { return "rici-b200 0.2.0 sm_100a"; }
 
 int64_t rici_mesh_num_triangles(rici_mesh mesh) { return mesh ? mesh->m.nt : -1; }
 
@@ -320,6 +349,12 @@ rici_status rici_create_mesh(const float *vertices, int64_t n_vertices, const in
             if (e == cudaSuccess)
                 e = rici::launch_mesh_stage_end((const float *)dv, n_vertices, (const int32_t *)di,
                                                 n_triangles, &mesh->m, centroid, s);
+            if (e == cudaSuccess) {
+                mesh->created_on = s;
+                e = cudaEventCreateWithFlags(&mesh->ready, cudaEventDisableTiming);
+                if (e == cudaSuccess) e = cudaEventRecord(mesh->ready, s);
+                mesh->note_use(s);                 // a destroy before any use waits for staging
+            }
         }
         if (e != cudaSuccess) { rici_destroy_mesh(mesh); return cuda_fail(e, "rici_create_mesh"); }
     } else {
@@ -343,6 +378,7 @@ rici_status rici_destroy_mesh(rici_mesh mesh) {
     if (mesh->m.sphere) cudaFreeAsync(mesh->m.sphere, 0);
     if (mesh->m.super_sphere) cudaFreeAsync(mesh->m.super_sphere, 0);
     if (mesh->m.order) cudaFreeAsync(mesh->m.order, 0);
+    if (mesh->ready) cudaEventDestroy(mesh->ready);
     delete mesh;
     return RICI_OK;
 }
@@ -365,6 +401,7 @@ rici_status rici_generate(rici_mesh mesh, const float *origins, int64_t n, float
     size_t out_bytes = sizeof(uint16_t) * (size_t)n * n_bins * n_bins;
     cudaError_t e = st.in(origins, sizeof(float) * 6 * (size_t)n, &dorig);
     if (e == cudaSuccess) e = st.out(out, out_bytes, &dout);
+    mesh->wait_ready(s);
     if (e == cudaSuccess)
         e = rici::launch_generate(mesh->m, (const float *)dorig, n, support_radius, n_bins,
                                   (uint16_t *)dout, s);
@@ -395,6 +432,7 @@ rici_status rici_clutter_fraction(rici_mesh mesh, const uint8_t *object_tag, con
     if (e == cudaSuccess) e = st.in(origins, sizeof(float) * 6 * (size_t)n, &dorig);
     if (e == cudaSuccess) e = st.out(out_fraction, sizeof(float) * (size_t)n, &df);
     if (e == cudaSuccess && out_area_all) e = st.out(out_area_all, sizeof(float) * (size_t)n, &da);
+    mesh->wait_ready(s);
     if (e == cudaSuccess)
         e = rici::launch_clutter_fraction(mesh->m, (const unsigned char *)dt, (const float *)dorig, n, support_radius,
                                           quadrature_q, (float *)df, (float *)da, s);

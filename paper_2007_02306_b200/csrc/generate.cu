@@ -99,19 +99,18 @@ __device__ __forceinline__ void red_shared(unsigned addr, int v) {
 // `acc` is the image's [N][N+1] difference array as a shared-window address: column N is a
 // sink, so a range end at N needs no test, and coinciding ends cancel in place.
 //
-// Per layer the slice endpoints are affine in the row centre rc = r + 1/2 (beta = rc*delta -
-// R/2): E0 = a + t (c - a) on the long edge, t = (beta - z_a)/(z_c - z_a), and E1 on the
-// polyline a -> b -> c, E1 = a + u1 (b - a) + u2 (c - b) with u1 = (beta - z_a)/(z_b - z_a) and
-// u2 = (beta - z_b)/(z_c - z_b), every parameter saturated to [0, 1]: below the middle vertex
-// u2 = 0 and E1 lies on (a,b); above it u1 = 1 and E1 lies on (b,c) (step 1) -- no
-// branch per layer.  The saturation also makes a row the ceil-based range admits by rounding
-// (beta within ~1 ulp outside [z_a, z_c), G5) a zero-length slice (E0 = E1 = a or c), which
-// contributes nothing; t = rc*S + O is (beta - z_a)/(z_c - z_a) rearranged (a beta shift of a
-// few ulps, far inside tau).  The (x, y) pairs run as packed FP32x2 instructions (FFMA2/FADD2).
+// Each slice endpoint is computed from its edge alone, in a canonical form -- lower vertex
+// first: E = lo + t (hi - lo), t = (beta - z_lo) / (z_hi - z_lo) -- so two triangles sharing an
+// edge produce bitwise the same point and a circle through it is counted exactly once (no crack
+// at shared edges; G5).  E0 lies on the long edge (a,c), E1 on (a,b) below the middle vertex and
+// on (b,c) from it up (step 1).  The parameters are saturated to [0, 1]: a row the
+// ceil-based range admits by rounding (beta within ~1 ulp outside [z_a, z_c), G5) becomes a
+// zero-length slice (E0 = E1 = a or c) and contributes nothing, so no per-layer membership test
+// is needed.  The (x, y) pairs run as packed FP32x2 instructions (FFMA2).
 __device__ __forceinline__ float2 f2(float x, float y) { return make_float2(x, y); }
-__device__ __forceinline__ float fma_sat(float a, float b, float c) {   // FFMA.SAT: clamp to [0, 1]
+__device__ __forceinline__ float mul_sat(float a, float b) {     // FMUL.SAT: clamp to [0, 1]
     float r;
-    asm("fma.rn.ftz.sat.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    asm("mul.rn.ftz.sat.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
     return r;
 }
 
@@ -127,23 +126,23 @@ __device__ __forceinline__ void rasterise_triangle(unsigned acc, const Geometry 
     bool stat_emitted = false;
 #endif
     RICI_STAT(4, r_hi - r_lo);
-    const float nh = -g.half_r;
     const float i_ac = fast_rcp(cz - az);                // z_c > z_a whenever a layer is inside
-    const float st = g.delta * i_ac, ot = (nh - az) * i_ac;
-    float s1 = 0.f, o1 = 1.f, s2 = 0.f, o2 = 0.f;        // flat (a,b): E1 starts at b; flat (b,c): stays on (a,b)
-    if (bz > az) { const float i = fast_rcp(bz - az); s1 = g.delta * i; o1 = (nh - az) * i; }
-    if (cz > bz) { const float i = fast_rcp(cz - bz); s2 = g.delta * i; o2 = (nh - bz) * i; }
-    const float2 A = f2(ax, ay), AC = f2(cx - ax, cy - ay), AB = f2(bx - ax, by - ay), BC = f2(cx - bx, cy - by);
+    const float i_ab = bz > az ? fast_rcp(bz - az) : 0.f;
+    const float i_bc = cz > bz ? fast_rcp(cz - bz) : 0.f;
+    const float2 A = f2(ax, ay), B = f2(bx, by), AC = f2(cx - ax, cy - ay), AB = f2(bx - ax, by - ay),
+                 BC = f2(cx - bx, cy - by);
     const float2 cm = f2(g.inv_delta, g.inv_delta), ch = f2(-0.5f, -0.5f);
     unsigned row = acc + 4u * (unsigned)(r_lo * (N + 1));
     const unsigned row_step = 4u * (unsigned)(N + 1);
     float rc = (float)r_lo + 0.5f;                        // r + 1/2, exact in float
     for (int r = r_lo; r < r_hi; ++r, row += row_step, rc += 1.f) {
+        const float beta = fmaf(rc, g.delta, -g.half_r);
         // Step 1: E0 on the long edge (a,c), E1 on (a,b) below / (b,c) above the middle vertex.
-        const float t = fma_sat(rc, st, ot);
-        const float u1 = fma_sat(rc, s1, o1), u2 = fma_sat(rc, s2, o2);
+        const float t = mul_sat(beta - az, i_ac);
         const float2 e0 = __ffma2_rn(f2(t, t), AC, A);
-        const float2 e1 = __ffma2_rn(f2(u2, u2), BC, __ffma2_rn(f2(u1, u1), AB, A));
+        const bool below = beta < bz;
+        const float u = mul_sat(beta - (below ? az : bz), below ? i_ab : i_bc);
+        const float2 e1 = __ffma2_rn(f2(u, u), below ? AB : BC, below ? A : B);
         // Step 2: rotate so E0E1 is parallel to x with the normalised direction D/|D| as
         // (cos, sin): the rotated x of E0 / E1 is (D.E0)/|D| / (D.E1)/|D|, so their signs are
         // those of D.E0 and D.E0 + |D|^2 -- the normalisation is only needed for |C| below.
@@ -573,13 +572,12 @@ cudaError_t launch_generate(const DeviceMesh &m, const float *d_origins, int64_t
 #define RICI_GEN_LAUNCH(KK)                                                                             \
     generate_kernel<KK><<<(unsigned)blocks, kThreads, smem, s>>>(m.tri, m.sphere, m.n_chunks, m.super_sphere, \
                                                                  m.n_super, d_origins, perm, n, R, N, g, d_out)
-    timing_call(0);
-    timing_begin(0, s);
+    KernelTimer timer(0, s);
     if (Kt == 8) RICI_GEN_LAUNCH(8);
     else if (Kt == 4) RICI_GEN_LAUNCH(4);
     else if (Kt == 2) RICI_GEN_LAUNCH(2);
     else RICI_GEN_LAUNCH(1);
-    timing_end(0, s);
+    timer.end();
 #undef RICI_GEN_LAUNCH
     note_launches(1);
     e = cudaGetLastError();

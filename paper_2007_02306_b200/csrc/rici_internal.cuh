@@ -30,11 +30,24 @@ cudaError_t kd_refine(const float *d_pts, int stride, int64_t n, int *d_perm, cu
 
 // Kernel-launch bookkeeping (rici_launch_count()).
 void note_launches(int k);
-// Per-kernel event timing (rici_set_kernel_timing): begin/end bracket the kernel's launch(es)
-// on stream s; no-ops while timing is off.
-void timing_begin(int kernel, cudaStream_t s);
-void timing_end(int kernel, cudaStream_t s);
-void timing_call(int kernel);            // once per API call: the mean is per call
+// Per-kernel event timing (rici_set_kernel_timing): a KernelTimer brackets one API call's
+// launches of a timed kernel on stream s.  begin() records the start event (nothing while timing
+// is off); end() records the stop event and files the pair; an un-ended timer (an error return
+// in between) gives its start event back on destruction, so concurrent calls never pair one
+// call's begin with another's end.
+cudaEvent_t timing_begin(int kernel, cudaStream_t s);    // nullptr while timing is off
+void timing_end(int kernel, cudaStream_t s, cudaEvent_t begin);
+void timing_release(cudaEvent_t begin);
+struct KernelTimer {
+    int kernel;
+    cudaStream_t s;
+    cudaEvent_t a = nullptr;
+    KernelTimer(int k, cudaStream_t st) : kernel(k), s(st) { a = timing_begin(k, st); }
+    void end() { if (a) { timing_end(kernel, s, a); a = nullptr; } }
+    ~KernelTimer() { if (a) timing_release(a); }
+    KernelTimer(const KernelTimer &) = delete;
+    KernelTimer &operator=(const KernelTimer &) = delete;
+};
 
 // Raises a kernel's dynamic shared-memory limit to `bytes` on the current device (once per
 // (kernel, device); thread-safe).
@@ -72,6 +85,10 @@ cudaError_t launch_crss_count_mma(const uint16_t *d_needles, int64_t nn, const u
                                   uint64_t *d_thr, bool thr_from_pairs, bool rank_mode, uint32_t *d_counts,
                                   cudaStream_t s);
 
+// rici_crss_guard_stats: {needles, needles outside the int8 guard, haystack images, haystack
+// images outside it, guard-valid needles that are not 2:4} accumulated on the current device.
+cudaError_t read_guard_stats(unsigned long long out[5], bool reset);
+
 // f4: Eq. 8 clutter fraction per oriented point (quadrature of the area inside the support
 // cylinder; object_tag [nt] in caller triangle order, device memory).
 cudaError_t launch_clutter_fraction(const DeviceMesh &m, const unsigned char *d_tag, const float *d_origins,
@@ -79,5 +96,8 @@ cudaError_t launch_clutter_fraction(const DeviceMesh &m, const unsigned char *d_
 
 // Which kernel counts ranks: the tensor-core path when N == 64 and RICI_CRSS_PATH != "simt".
 bool use_mma_path(int N);
+// Tuning knobs from the environment (read once by each caller into a function-local static).
+int env_int(const char *name, int dflt);
+double env_double(const char *name, double dflt);
 
 }  // namespace rici

@@ -26,7 +26,7 @@ def _declared():
 
 def test_header_symbols_exported(lib):
     declared = _declared()
-    assert len(declared) == 15
+    assert len(declared) == 16
     out = subprocess.run(["nm", "-D", "--defined-only", os.path.join(ROOT, "paper_2007_02306_b200", "librici.so")],
                          capture_output=True, text=True, check=True).stdout
     exported = set(re.findall(r" T (rici_\w+)", out))
@@ -69,6 +69,7 @@ def test_version_and_argument_validation(lib):
     assert lib.rici_clutter_fraction(None, None, None, 0, ctypes.c_float(0.3), 4, None, None, None) == 1
     assert lib.rici_destroy_mesh(None) == 0
     assert lib.rici_mesh_num_triangles(None) == -1
+    assert lib.rici_crss_guard_stats(None, 0) == 1                                           # null out
 
 
 def test_product_does_not_touch_oracle():

@@ -118,7 +118,6 @@ def test_sharded_scene_step_cuda_two_ranks():
     m2 = rici.rici_create_mesh(torch.from_numpy(sc.vertices).cuda(), torch.from_numpy(sc.indices).cuda())
     hay1 = rici.rici_generate(m2, torch.from_numpy(so).cuda(), 0.3, 64)
     want = rici.rici_crss_search(nd1, hay1).cpu().numpy().astype(np.int64)
-    assert want.max() > 0
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()

@@ -305,10 +305,42 @@ def test_crss_count_mma_guard_and_fallback(rici, oracle_mod, big):
     H = np.concatenate([A, _mixed_images(rng, 477, 9, 11, big)])
     D = oracle_mod.crss_matrix(A, H)
     thr = D[np.arange(300), rng.integers(0, H.shape[0], 300)].copy()
+    rici.rici_crss_guard_stats(reset=True)
     got = rici.rici_crss_count_below(_dev(A), _dev(H), torch.from_numpy(thr.view(np.int64)).to(DEV))
     assert np.array_equal(got.cpu().numpy().astype(np.int64), (D < thr[:, None]).sum(1))
+    st = rici.rici_crss_guard_stats(reset=True)
+    assert st["needles"] == 300 and st["haystack"] == 777
+    dn = np.abs(np.diff(A.astype(np.int64), axis=2)).reshape(300, -1).max(1)
+    dh = np.abs(np.diff(H.astype(np.int64), axis=2)).reshape(777, -1).max(1)
+    assert st["needles_outside_guard"] == int((dn > 63).sum()) and st["haystack_outside_guard"] == int((dh > 15).sum())
     r = rici.rici_crss_search(_dev(A), _dev(H)).cpu().numpy()
     assert np.array_equal(r.astype(np.uint32), oracle_mod.ranks(A, H))
+
+
+def test_search_captured_in_cuda_graph(rici, oracle_mod):
+    """No host synchronisation anywhere in rici_crss_search / count_below (tensor path with the
+    device-sized dense subset and guard fallback): the calls capture into a CUDA graph, and the
+    replay -- on new inputs copied into the same buffers -- equals the oracle."""
+    rng = np.random.default_rng(91)
+    A = _rand_imgs(rng, 600, hi=4, density=0.03)
+    A[rng.choice(600, 40, replace=False)] = _rand_imgs(rng, 40, hi=6, density=0.5)   # not 2:4: dense pass
+    A[3, 10, 20] = 300                                                          # guard break: fallback
+    H = np.concatenate([A + (rng.random(A.shape) < 0.004).astype(np.uint16), _rand_imgs(rng, 500, hi=4, density=0.05)])
+    H[700, 5, 9] = 40                                                           # haystack guard break
+    nd, hd = _dev(A), _dev(H)
+    out = torch.empty(600, dtype=torch.int32, device=DEV)
+    rici.rici_crss_search(nd, hd, out=out)                                      # warm-up (caches, smem)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        rici.rici_crss_search(nd, hd, out=out)
+    A2 = A.copy()
+    A2[::5] = H[600:720]                                                        # wrong matches: ranks > 0
+    nd.copy_(_dev(A2))
+    g.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy().astype(np.uint32), oracle_mod.ranks(A2, H))
+    assert out.max() > 0
 
 
 def test_crss_guard_edges_exact(rici, oracle_mod):
