@@ -337,6 +337,26 @@ def extra_c2(rici, torch, dev, stream, flush, reps=5, simt=True):
     return res
 
 
+def extra_rank_mode(rici, torch, needles, hay, ranks_full, stream, flush, reps=3):
+    """The same C4 search in rank mode (RICI_CRSS_EARLY_EXIT: tiles retired once a K-prefix
+    lower bound reaches t_i): identical ranks, fewer MMAs."""
+    out = torch.empty_like(ranks_full)
+    ts = []
+    for it in range(reps + 1):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        rici.rici_crss_search(needles, hay, out=out, early_exit=True)
+        b.record(stream)
+        torch.cuda.synchronize()
+        if it:
+            ts.append(a.elapsed_time(b))
+    ms = float(np.mean(ts))
+    cmp = float(needles.shape[0]) * hay.shape[0]
+    return {"ms": ms, "comparisons_per_s": cmp / (ms / 1e3), "ranks_equal_full_mode": bool(torch.equal(out, ranks_full)),
+            "reps": reps, "note": "rici_crss_search(early_exit=True) on the step's needles and haystack"}
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
@@ -400,6 +420,7 @@ def run_gpu(args):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    rici.rici_crss_guard_stats(reset=True)
     launches0 = rici.rici_launch_count()
     for kid in (0, 1):                         # clear, then time the kernels' own launches live
         rici.rici_kernel_time_ms(kid)
@@ -418,6 +439,12 @@ def run_gpu(args):
         wall = time.perf_counter() - t0
     launches = rici.rici_launch_count() - launches0
     rici.rici_set_kernel_timing(False)
+    gs = rici.rici_crss_guard_stats(reset=True)
+    guard = {"needles_outside_int8_guard": gs["needles_outside_guard"] / max(gs["needles"], 1),
+             "haystack_outside_int8_guard": gs["haystack_outside_guard"] / max(gs["haystack"], 1),
+             "needles_not_2_4": gs["needles_not_2_4"] / max(gs["needles"], 1),
+             "note": "fractions over the timed searches: outside the guard -> exact SIMT fallback; "
+                     "guard-valid but not 2:4 -> dense tcgen05 kernel on the side stream"}
     gen_kernel_ms, n_gen_k = rici.rici_kernel_time_ms(0)       # generate_kernel, per call (2 per step)
     mma_kernel_ms, n_mma_k = rici.rici_kernel_time_ms(1)       # tcgen05 GEMM launches, per search call
 
@@ -540,6 +567,7 @@ def run_gpu(args):
 
     extras = {}
     if world == 1 and not args.no_extras:
+        extras["c4_rank_mode_search"] = extra_rank_mode(rici, torch, needles, hay, ranks_d, stream, flush)
         del hay
         torch.cuda.empty_cache()
         extras["c3_construction"] = extra_c3(rici, torch, dev, stream, flush)
@@ -556,7 +584,8 @@ def run_gpu(args):
             "comparisons_per_s": comparisons / (step_ms / 1e3),
             "construction": construction,
             "crss": {"ms": crss_ms, "comparisons_per_s": comparisons / (crss_ms / 1e3), "mode": "full",
-                     "rank0_fraction": rank0_frac, "ranks_identical_on_all_ranks": ranks_ok},
+                     "rank0_fraction": rank0_frac, "ranks_identical_on_all_ranks": ranks_ok,
+                     "guard": guard},
             "roofline": roof, "cpu_baseline": cb, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk.summary(), "bench_wall_s": wall, "rank0_local_step_ms": local_step}
     line.update(extras)
