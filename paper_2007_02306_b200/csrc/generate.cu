@@ -39,7 +39,7 @@ namespace rici {
 namespace {
 
 #if RICI_GEN_STATS   // tuning builds only: event counters read by rici_debug_gen_stats
-__device__ unsigned long long g_stats[10];
+__device__ unsigned long long g_stats[12];
 #define RICI_STAT(i, v) atomicAdd(&g_stats[i], (unsigned long long)(v))
 #else
 #define RICI_STAT(i, v)
@@ -50,18 +50,10 @@ constexpr int kMaxK = 8;
 constexpr int kListCap = 2 * kThreads;   // superchunk survivors per batch
 constexpr int kChunkCap = 1024;          // chunk survivors per batch (multiple of kSuper)
 
-// First index i in [0, n] with (i + 1/2) * delta + off >= v, i.e. ceil(v/delta - off/delta - 1/2).
-// Used for rows (off = -R/2: beta_r >= v) and columns (off = 0: rho_c >= v).  Exact ties are
-// fragile pixels; the row loop re-checks membership with explicit comparisons.
-// cvt.rpi.s32.f32 is ceil with saturation (NaN -> 0), so one conversion replaces clamp + ceil.
-__device__ __forceinline__ int first_at_or_above(float v, float inv_delta, float off_scaled, int n) {
-    const int i = __float2int_ru(fmaf(v, inv_delta, off_scaled));   // v/delta - off/delta - 1/2
-    return min(max(i, 0), n);
-}
-// The same for v >= 0 and off = 0 (columns): the argument is >= -1/2, so the ceiling is >= 0.
-__device__ __forceinline__ int first_col_at_or_above(float v, float inv_delta, int n) {
-    return min(__float2int_ru(fmaf(v, inv_delta, -0.5f)), n);
-}
+// Bin indices in the bin-unit frame (rasterise_triangle): the first row r with Z_r = r >= v is
+// ceil(v), the first column whose circle (radius c + 1/2) is at or beyond v is ceil(v - 1/2);
+// cvt.rpi.s32.f32 (__float2int_ru) is ceil with saturation (NaN -> 0).  Exact ties are fragile
+// pixels (G5).
 
 __device__ __forceinline__ void sort3(float &ax, float &ay, float &az, float &bx, float &by,
                                       float &bz, float &cx, float &cy, float &cz) {
@@ -114,13 +106,21 @@ __device__ __forceinline__ float mul_sat(float a, float b) {     // FMUL.SAT: cl
     return r;
 }
 
-__device__ __forceinline__ void rasterise_triangle(unsigned acc, const Geometry &g,
+#ifndef RICI_GEN_RED_MODE
+#define RICI_GEN_RED_MODE 1     // C4 341 -> 337 ms against the branch on an empty range (r2d)
+#endif
+
+// All coordinates here are in BIN units (DESIGN.md 6.1 "bin-unit frame"): x, y scaled by
+// 1/delta = N/R, and Z = z/delta + N/2 - 1/2, so layer r lies at Z = r exactly (beta_r =
+// (r + 1/2) delta - R/2, G4), column c's circle at radius c + 1/2, and the support radius is N.
+template <int NC>
+__device__ __forceinline__ void rasterise_triangle(unsigned acc, int n_rt,
                                                    float ax, float ay, float az, float bx,
                                                    float by, float bz, float cx, float cy,
                                                    float cz) {
-    const int N = g.n;
-    const int r_lo = first_at_or_above(az, g.inv_delta, g.row_off, N);
-    const int r_hi = first_at_or_above(cz, g.inv_delta, g.row_off, N);
+    const int N = NC ? NC : n_rt;
+    const int r_lo = min(max(__float2int_ru(az), 0), N);     // first row with Z_r >= z_a
+    const int r_hi = min(max(__float2int_ru(cz), 0), N);
     if (r_lo >= r_hi) { RICI_STAT(8, 1); return; }
 #if RICI_GEN_STATS
     bool stat_emitted = false;
@@ -131,17 +131,16 @@ __device__ __forceinline__ void rasterise_triangle(unsigned acc, const Geometry 
     const float i_bc = cz > bz ? fast_rcp(cz - bz) : 0.f;
     const float2 A = f2(ax, ay), B = f2(bx, by), AC = f2(cx - ax, cy - ay), AB = f2(bx - ax, by - ay),
                  BC = f2(cx - bx, cy - by);
-    const float2 cm = f2(g.inv_delta, g.inv_delta), ch = f2(-0.5f, -0.5f);
-    unsigned row = acc + 4u * (unsigned)(r_lo * (N + 1));
+    const float2 half = f2(-0.5f, -0.5f);
     const unsigned row_step = 4u * (unsigned)(N + 1);
-    float rc = (float)r_lo + 0.5f;                        // r + 1/2, exact in float
-    for (int r = r_lo; r < r_hi; ++r, row += row_step, rc += 1.f) {
-        const float beta = fmaf(rc, g.delta, -g.half_r);
+    unsigned row = acc + row_step * (unsigned)r_lo;
+    const float rz_hi = (float)r_hi;
+    for (float rz = (float)r_lo; rz < rz_hi; rz += 1.f, row += row_step) {
         // Step 1: E0 on the long edge (a,c), E1 on (a,b) below / (b,c) above the middle vertex.
-        const float t = mul_sat(beta - az, i_ac);
+        const float t = mul_sat(rz - az, i_ac);
         const float2 e0 = __ffma2_rn(f2(t, t), AC, A);
-        const bool below = beta < bz;
-        const float u = mul_sat(beta - (below ? az : bz), below ? i_ab : i_bc);
+        const bool below = rz < bz;
+        const float u = mul_sat(rz - (below ? az : bz), below ? i_ab : i_bc);
         const float2 e1 = __ffma2_rn(f2(u, u), below ? AB : BC, below ? A : B);
         // Step 2: rotate so E0E1 is parallel to x with the normalised direction D/|D| as
         // (cos, sin): the rotated x of E0 / E1 is (D.E0)/|D| / (D.E1)/|D|, so their signs are
@@ -149,29 +148,40 @@ __device__ __forceinline__ void rasterise_triangle(unsigned acc, const Geometry 
         const float2 d = __ffma2_rn(e0, f2(-1.f, -1.f), e1);
         const float l2 = fmaf(d.x, d.x, d.y * d.y);
         const float de0 = fmaf(d.x, e0.x, d.y * e0.y);    // |D| * x0
-        // Steps 3-4: distances of E0, E1 from the axis; single range [min, max).
+        // Steps 3-4: distances of E0, E1 from the axis; single range [min, max).  Column c's
+        // circle (radius c + 1/2 in bin units) is the first at or beyond v at ceil(v - 1/2).
         const float r0 = fast_sqrt(fmaf(e0.x, e0.x, e0.y * e0.y)), r1 = fast_sqrt(fmaf(e1.x, e1.x, e1.y * e1.y));
-        const float2 cf = __ffma2_rn(f2(fminf(r0, r1), fmaxf(r0, r1)), cm, ch);   // v/delta - 1/2
+        const float2 cf = __fadd2_rn(f2(fminf(r0, r1), fmaxf(r0, r1)), half);
         const int c_min = min(__float2int_ru(cf.x), N), c_max = min(__float2int_ru(cf.y), N);
         // Steps 5-6: double range [|C|, min) iff the x signs differ (x = 0 non-negative);
         // |C| = |rotated y| = |D x E0| / |D|.  Single: +1 at c_min, -1 at c_max.  Double:
         // +2 at c_c, -1 at c_min, -1 at c_max.  Empty ranges (also a zero-length slice, whose
-        // r0 = r1 and de0 = 0) cancel at one address.
+        // r0 = r1 and de0 = 0) cancel at one address; they are predicated off.
         const bool dbl = de0 < 0.f && de0 + l2 >= 0.f;
         int c_lo = c_min;
         if (dbl) {
             const float y = fmaf(d.x, e0.y, -d.y * e0.x) * rsqrtf(l2);
-            c_lo = min(first_col_at_or_above(fabsf(y), g.inv_delta, N), c_min);
+            c_lo = min(min(__float2int_ru(fabsf(y) - 0.5f), N), c_min);
         }
-        if (c_lo == c_max) continue;                      // nothing in [c_lo, c_max)
-        RICI_STAT(5, 1);
+        const bool emit = c_lo != c_max;                  // something in [c_lo, c_max)
+        RICI_STAT(5, emit ? 1 : 0);
 #if RICI_GEN_STATS
-        stat_emitted = true;
+        stat_emitted |= emit;
 #endif
+#if RICI_GEN_RED_MODE == 1
+        // unconditional: +v1 at c_lo, +v2 at c_min, -1 at c_max with (v1, v2) = (2, -1) for a
+        // double range and (1, 0) for a single one; an empty range cancels in place
+        red_shared(row + 4u * (unsigned)c_lo, dbl ? 2 : 1);
+        red_shared(row + 4u * (unsigned)c_min, dbl ? -1 : 0);
+        red_shared(row + 4u * (unsigned)c_max, -1);
+    }
+#else
+        if (!emit) continue;
         red_shared(row + 4u * (unsigned)c_lo, dbl ? 2 : 1);
         if (dbl) red_shared(row + 4u * (unsigned)c_min, -1);
         red_shared(row + 4u * (unsigned)c_max, -1);
     }
+#endif
 #if RICI_GEN_STATS
     if (!stat_emitted) RICI_STAT(9, 1);            // rasterised pairs that emitted no segment
 #endif
@@ -180,30 +190,44 @@ __device__ __forceinline__ void rasterise_triangle(unsigned acc, const Geometry 
 // Work item of the survivor queue: (chunk, triangle lane, image) packed in 32 bits.
 __device__ __forceinline__ int pack_item(int64_t chunk, int t, int k) { return (int)(chunk << 8) | (t << 3) | k; }
 
-// Project one triangle into image k's spin frame (Eqs. 2-4) and, when its beta-extent
-// holds at least one layer, rasterise it.  The same arithmetic decides the cull (in the
-// queue phase) and the rasterisation, so the two can never disagree.
-__device__ __forceinline__ void project_z(const Frame &f, const float *v, float *p, float *z) {
+// The per-image projection in bin units: translation first (Eq. 2, S_v), then the composed
+// rotation of Eqs. 3-4 scaled by 1/delta, with the row offset folded into Z.
+struct __align__(16) GenFrame {
+    float sx, sy, sz, zoff;      // S_v; N/2 - 1/2
+    float xx, xy, xz, yx;        // X = xx px + xy py + xz pz;  Y = yx px + yy py
+    float yy, zx, zy, zz;        // Z = zx px + zy py + zz pz + zoff
+};
+__device__ __forceinline__ GenFrame gen_frame(const Frame &f, float inv_delta, float zoff) {
+    GenFrame q;
+    q.sx = f.sx; q.sy = f.sy; q.sz = f.sz; q.zoff = zoff;
+    q.xx = f.nbz * f.nax * inv_delta; q.xy = f.nbz * f.nay * inv_delta; q.xz = -f.nbx * inv_delta;
+    q.yx = -f.nay * inv_delta; q.yy = f.nax * inv_delta;
+    q.zx = f.czx * inv_delta; q.zy = f.czy * inv_delta; q.zz = f.czz * inv_delta;
+    return q;
+}
+
+// Project one triangle into image k's spin frame (Eqs. 2-4); the same arithmetic decides the
+// cull (in the queue phase) and the rasterisation, so the two can never disagree.
+__device__ __forceinline__ void project_z(const GenFrame &f, const float *v, float *p, float *z) {
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
         p[3 * j] = v[3 * j] - f.sx;                     // Eq. 2: translate first
         p[3 * j + 1] = v[3 * j + 1] - f.sy;
         p[3 * j + 2] = v[3 * j + 2] - f.sz;
-        z[j] = fmaf(f.czx, p[3 * j], fmaf(f.czy, p[3 * j + 1], f.czz * p[3 * j + 2]));   // T_z
+        z[j] = fmaf(f.zx, p[3 * j], fmaf(f.zy, p[3 * j + 1], fmaf(f.zz, p[3 * j + 2], f.zoff)));   // T_z
     }
 }
 
 // Eqs. 3-4 for T_x, T_y of the three translated vertices p (project_z output).
-__device__ __forceinline__ void project_xy(const Frame &f, const float *p, float *x, float *y) {
+__device__ __forceinline__ void project_xy(const GenFrame &f, const float *p, float *x, float *y) {
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
-        float qx = fmaf(f.nax, p[3 * j], f.nay * p[3 * j + 1]);
-        y[j] = fmaf(-f.nay, p[3 * j], f.nax * p[3 * j + 1]);
-        x[j] = fmaf(f.nbz, qx, -f.nbx * p[3 * j + 2]);
+        y[j] = fmaf(f.yx, p[3 * j], f.yy * p[3 * j + 1]);
+        x[j] = fmaf(f.xx, p[3 * j], fmaf(f.xy, p[3 * j + 1], f.xz * p[3 * j + 2]));
     }
 }
-// alpha cull: if the triangle's (T_x, T_y) bounding box misses the disk of radius R, every
-// slice point has alpha > R > rho_{N-1} and no bin can be hit (exact skip)
+// alpha cull: if the triangle's (T_x, T_y) bounding box misses the support disk (radius N in
+// bin units), every slice point has alpha > R > rho_{N-1} and no bin can be hit (exact skip)
 __device__ __forceinline__ bool alpha_box_hits(const float *x, const float *y, float r2) {
     const float bx0 = fmaxf(fmaxf(fminf(x[0], fminf(x[1], x[2])), -fmaxf(x[0], fmaxf(x[1], x[2]))), 0.f);
     const float by0 = fmaxf(fmaxf(fminf(y[0], fminf(y[1], y[2])), -fmaxf(y[0], fmaxf(y[1], y[2]))), 0.f);
@@ -216,11 +240,12 @@ __device__ __forceinline__ bool alpha_box_hits(const float *x, const float *y, f
 #define RICI_GEN_ALPHA_EARLY 1
 #endif
 
-// K <= 2 (N = 64 default): 32 KB of counters, so smem admits 5 CTAs / SM; cap the registers
-// (48, a few bytes of spill) so the register file admits them too -- measured 3.34 -> 3.09 ms on C2
-template <int K>
+// K <= 2 (N = 64 default): 33 KB of counters per CTA.  With the bin-unit frame, 4 CTAs / SM at
+// 60 registers (no spill) beat 5 CTAs at the 48-register cap (spills): C4 337 -> 325 ms, C3 103 ->
+// 99 ms, C2 1.75 -> 1.70 ms (r2e).  Round 1, before the bin-unit frame, had measured 5 > 4.
+template <int K, int NC>
 #ifndef RICI_GEN_MIN_BLOCKS
-#define RICI_GEN_MIN_BLOCKS 5
+#define RICI_GEN_MIN_BLOCKS 4
 #endif
 __global__ void __launch_bounds__(kThreads, K <= 2 ? RICI_GEN_MIN_BLOCKS : 1)
 generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere, int64_t n_chunks,
@@ -229,6 +254,7 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
                 float R, int N, const Geometry g, uint16_t *__restrict__ out) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ Frame frames[kMaxK];
+    __shared__ GenFrame gframes[kMaxK];
     __shared__ int img_idx[kMaxK];
     __shared__ int list[kListCap];
     __shared__ int list_n, chunk_n;
@@ -238,6 +264,7 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
 
     int *acc = reinterpret_cast<int *>(smem_raw);        // [K][N][N+1] difference arrays
     const unsigned acc_s = (unsigned)__cvta_generic_to_shared(acc);
+    if (NC) N = NC;                                      // N = 64: compile-time bin geometry
     const int img_words = N * (N + 1);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned lt_mask = (1u << lane) - 1u;
@@ -255,9 +282,11 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
             const int idx = img_perm ? img_perm[img0 + tid] : (int)(img0 + tid);
             img_idx[tid] = idx;
             frames[tid] = make_frame(origins + 6 * (int64_t)idx);
+            gframes[tid] = gen_frame(frames[tid], g.inv_delta, g.row_off);
         } else {
             Frame f = {};
             frames[tid] = f;
+            gframes[tid] = gen_frame(f, g.inv_delta, g.row_off);
         }
     }
     __syncthreads();
@@ -309,21 +338,20 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
             float v[9];
 #pragma unroll
             for (int c = 0; c < 9; ++c) v[c] = __ldg(src + c * kChunk);
-            const Frame f = frames[k];
+            const GenFrame f = gframes[k];
             float p[9], z[3];
             project_z(f, v, p, z);
             float x[3], y[3];
             project_xy(f, p, x, y);                      // Eqs. 3-4 for T_x, T_y
-            if (RICI_GEN_ALPHA_EARLY || alpha_box_hits(x, y, g.r2)) {
+            if (RICI_GEN_ALPHA_EARLY || alpha_box_hits(x, y, (float)(N * N))) {
                 RICI_STAT(3, 1);
                 float ax = x[0], ay = y[0], az = z[0], bx = x[1], by = y[1], bz = z[1],
                       cx = x[2], cy = y[2], cz = z[2];
                 sort3(ax, ay, az, bx, by, bz, cx, cy, cz);
 #if RICI_GEN_STATS
-                stat_rows = max(0, first_at_or_above(cz, g.inv_delta, g.row_off, g.n) -
-                                       first_at_or_above(az, g.inv_delta, g.row_off, g.n));
+                stat_rows = max(0, min(max(__float2int_ru(cz), 0), N) - min(max(__float2int_ru(az), 0), N));
 #endif
-                rasterise_triangle(acc_s + 4u * (unsigned)(k * img_words), g, ax, ay, az, bx, by, bz, cx, cy, cz);
+                rasterise_triangle<NC>(acc_s + 4u * (unsigned)(k * img_words), N, ax, ay, az, bx, by, bz, cx, cy, cz);
             }
         }
 #if RICI_GEN_STATS
@@ -425,25 +453,66 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
                     // lie in [z_min, z_max)?  Survivors go to the warp's queue.
                     // the K images' tests are independent chains: computed together (ILP), then
                     // pushed in image order
+#if RICI_GEN_STATS
+                    {   // finer culls, counted only: the 8-triangle sub-chunk's sphere and the triangle's
+                        // own sphere against each tested image's support cylinder (stats 10, 11)
+                        float tc[3], tr = 0.f;
+                        for (int a = 0; a < 3; ++a) tc[a] = (v[a] + v[3 + a] + v[6 + a]) * (1.f / 3.f);
+                        for (int j = 0; j < 3; ++j) {
+                            float dx = v[3 * j] - tc[0], dy = v[3 * j + 1] - tc[1], dz = v[3 * j + 2] - tc[2];
+                            tr = fmaxf(tr, sqrtf(dx * dx + dy * dy + dz * dz));
+                        }
+                        float lo[3], hi[3];
+                        for (int a = 0; a < 3; ++a) { lo[a] = tc[a] - tr; hi[a] = tc[a] + tr; }
+                        for (int o = 1; o < 8; o <<= 1)
+                            for (int a = 0; a < 3; ++a) {
+                                lo[a] = fminf(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+                                hi[a] = fmaxf(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+                            }
+                        float sc[3], sr = 0.f;
+                        for (int a = 0; a < 3; ++a) sc[a] = 0.5f * (lo[a] + hi[a]);
+                        {
+                            float dx = tc[0] - sc[0], dy = tc[1] - sc[1], dz = tc[2] - sc[2];
+                            sr = sqrtf(dx * dx + dy * dy + dz * dz) + tr;
+                        }
+                        for (int o = 1; o < 8; o <<= 1) sr = fmaxf(sr, __shfl_xor_sync(0xffffffffu, sr, o));
+                        for (int k = 0; k < K; ++k) {
+                            if (!((kmask >> k) & 1u)) continue;
+                            const Frame &f = frames[k];
+                            auto cyl = [&](const float *c, float w) {
+                                const float pad = 1e-4f * R + 1e-6f * (fabsf(c[0]) + fabsf(c[1]) + fabsf(c[2]) + w);
+                                const float ra = R + w + pad, hb = 0.5f * R + w + pad;
+                                float ex = c[0] - f.sx, ey = c[1] - f.sy, ez = c[2] - f.sz;
+                                float b = fmaf(f.czx, ex, fmaf(f.czy, ey, f.czz * ez));
+                                float a2 = fmaxf(ex * ex + ey * ey + ez * ez - b * b, 0.f);
+                                return fabsf(b) <= hb && a2 <= ra * ra;
+                            };
+                            RICI_STAT(10, cyl(sc, sr) ? 1 : 0);
+                            RICI_STAT(11, cyl(tc, tr) ? 1 : 0);
+                        }
+                    }
+#endif
                     bool keep[K];
+                    {
 #pragma unroll
                     for (int k = 0; k < K; ++k) {
                         keep[k] = false;
                         if ((kmask >> k) & 1u) {
-                            const Frame f = frames[k];
+                            const GenFrame f = gframes[k];
                             float p[9], z[3];
                             project_z(f, v, p, z);
                             float zlo = fminf(z[0], fminf(z[1], z[2])), zhi = fmaxf(z[0], fmaxf(z[1], z[2]));
-                            keep[k] = first_at_or_above(zlo, g.inv_delta, g.row_off, N) <
-                                      first_at_or_above(zhi, g.inv_delta, g.row_off, N);
+                            // a layer Z = r (integer) in [zlo, zhi) within [0, N)
+                            keep[k] = min(max(__float2int_ru(zlo), 0), N) < min(max(__float2int_ru(zhi), 0), N);
 #if RICI_GEN_ALPHA_EARLY
                             if (keep[k]) {
                                 float x[3], y[3];
                                 project_xy(f, p, x, y);
-                                keep[k] = alpha_box_hits(x, y, g.r2);
+                                keep[k] = alpha_box_hits(x, y, (float)(N * N));
                             }
 #endif
                         }
+                    }
                     }
 #pragma unroll
                     for (int k = 0; k < K; ++k) {
@@ -543,9 +612,11 @@ cudaError_t launch_generate(const DeviceMesh &m, const float *d_origins, int64_t
     if (n == 0) return cudaSuccess;
     const int K = generate_images_per_cta(N);
     size_t smem = (size_t)K * N * (N + 1) * sizeof(int);
-    const void *kern = K >= 8 ? (const void *)generate_kernel<8> : K >= 4 ? (const void *)generate_kernel<4>
-                     : K >= 2 ? (const void *)generate_kernel<2> : (const void *)generate_kernel<1>;
     const int Kt = K >= 8 ? 8 : K >= 4 ? 4 : K >= 2 ? 2 : 1;
+    const bool n64 = N == 64 && Kt == 2;                  // the compile-time N = 64 instance
+    const void *kern = n64 ? (const void *)generate_kernel<2, 64>
+                     : Kt == 8 ? (const void *)generate_kernel<8, 0> : Kt == 4 ? (const void *)generate_kernel<4, 0>
+                     : Kt == 2 ? (const void *)generate_kernel<2, 0> : (const void *)generate_kernel<1, 0>;
     smem = (size_t)Kt * N * (N + 1) * sizeof(int);
     {
         cudaError_t e = ensure_smem(kern, smem);
@@ -555,11 +626,11 @@ cudaError_t launch_generate(const DeviceMesh &m, const float *d_origins, int64_t
     int *perm = nullptr;
     cudaError_t e = cudaMallocAsync((void **)&perm, sizeof(int) * n, s);
     if (e != cudaSuccess) return e;
-    if ((e = spatial_order(d_origins, 6, n, perm, s)) != cudaSuccess) return e;
+    if ((e = spatial_order(d_origins, 6, n, perm, s)) != cudaSuccess) { cudaFreeAsync(perm, s); return e; }
 #ifndef RICI_GEN_KD_IMAGES
 #define RICI_GEN_KD_IMAGES 0
 #endif
-    if (RICI_GEN_KD_IMAGES && (e = kd_refine(d_origins, 6, n, perm, s)) != cudaSuccess) return e;
+    if (RICI_GEN_KD_IMAGES && (e = kd_refine(d_origins, 6, n, perm, s)) != cudaSuccess) { cudaFreeAsync(perm, s); return e; }
     int64_t blocks = (n + Kt - 1) / Kt;
     // the geometry lives in the kernel's parameter bank (no per-thread recomputation)
     Geometry g;
@@ -569,14 +640,15 @@ cudaError_t launch_generate(const DeviceMesh &m, const float *d_origins, int64_t
     g.half_r = 0.5f * R;
     g.r2 = R * R;
     g.row_off = 0.5f * (float)N - 0.5f;
-#define RICI_GEN_LAUNCH(KK)                                                                             \
-    generate_kernel<KK><<<(unsigned)blocks, kThreads, smem, s>>>(m.tri, m.sphere, m.n_chunks, m.super_sphere, \
+#define RICI_GEN_LAUNCH(KK, NN)                                                                         \
+    generate_kernel<KK, NN><<<(unsigned)blocks, kThreads, smem, s>>>(m.tri, m.sphere, m.n_chunks, m.super_sphere, \
                                                                  m.n_super, d_origins, perm, n, R, N, g, d_out)
     KernelTimer timer(0, s);
-    if (Kt == 8) RICI_GEN_LAUNCH(8);
-    else if (Kt == 4) RICI_GEN_LAUNCH(4);
-    else if (Kt == 2) RICI_GEN_LAUNCH(2);
-    else RICI_GEN_LAUNCH(1);
+    if (n64) RICI_GEN_LAUNCH(2, 64);
+    else if (Kt == 8) RICI_GEN_LAUNCH(8, 0);
+    else if (Kt == 4) RICI_GEN_LAUNCH(4, 0);
+    else if (Kt == 2) RICI_GEN_LAUNCH(2, 0);
+    else RICI_GEN_LAUNCH(1, 0);
     timer.end();
 #undef RICI_GEN_LAUNCH
     note_launches(1);
@@ -590,8 +662,8 @@ cudaError_t launch_generate(const DeviceMesh &m, const float *d_origins, int64_t
 #if RICI_GEN_STATS
 extern "C" __attribute__((visibility("default"))) int rici_debug_gen_stats(unsigned long long *out, int reset) {
     cudaDeviceSynchronize();
-    cudaMemcpyFromSymbol(out, rici::g_stats, sizeof(unsigned long long) * 10);
-    if (reset) { unsigned long long z[10] = {}; cudaMemcpyToSymbol(rici::g_stats, z, sizeof(z)); }
+    cudaMemcpyFromSymbol(out, rici::g_stats, sizeof(unsigned long long) * 12);
+    if (reset) { unsigned long long z[12] = {}; cudaMemcpyToSymbol(rici::g_stats, z, sizeof(z)); }
     return 0;
 }
 #endif
