@@ -164,6 +164,7 @@ __device__ __forceinline__ void rasterise_triangle(unsigned acc, int n_rt,
             c_lo = min(min(__float2int_ru(fabsf(y) - 0.5f), N), c_min);
         }
         const bool emit = c_lo != c_max;                  // something in [c_lo, c_max)
+        (void)emit;
         RICI_STAT(5, emit ? 1 : 0);
 #if RICI_GEN_STATS
         stat_emitted |= emit;
@@ -233,7 +234,6 @@ __device__ __forceinline__ bool alpha_box_hits(const float *x, const float *y, f
     const float by0 = fmaxf(fmaxf(fminf(y[0], fminf(y[1], y[2])), -fmaxf(y[0], fmaxf(y[1], y[2]))), 0.f);
     return bx0 * bx0 + by0 * by0 <= r2;
 }
-
 // RICI_GEN_ALPHA_EARLY: the alpha-box test runs in the queue phase (with the beta-extent test),
 // so only pairs with rasterisation work are queued and every drained lane has a triangle
 #ifndef RICI_GEN_ALPHA_EARLY
