@@ -11,19 +11,21 @@
 //   3. increment the bins whose circle radius falls in those ranges.
 //
 // B200 design:
-//  * one CTA owns K images (K = 2 at N = 64, 5 CTAs / SM); their 32-bit counters live in
+//  * one CTA owns K images (K = 2 at N = 64, 3 CTAs / SM); their 32-bit counters live in
 //    shared memory as per-row DIFFERENCE arrays of N+1 columns (column N a sink), so a
-//    segment costs <= 3 branch-free shared reductions (+2 at col(|C|), -1 at col(min), -1 at
-//    col(max)) instead of one per covered bin; a warp-shuffle prefix scan per row turns them
-//    into counts in the epilogue;
+//    segment costs 3 branch-free shared reductions (+2 at col(|C|), -1 at col(min), -1 at
+//    col(max)) instead of one per covered bin; a per-row prefix scan in the epilogue turns
+//    them into counts;
+//  * every image's frame is pre-scaled to BIN units (layer r at Z = r, column c's circle at
+//    radius c + 1/2), after the translation of Eq. 2;
 //  * images are built in spatial (Hilbert-cell) order and the mesh is stored in spatially
 //    compact chunks of 32 triangles (mesh.cu, sort.cu); an exact three-level cull skips
 //    triangles that cannot reach any of the CTA's support volumes: superchunk spheres and
 //    chunk spheres vs the CTA sphere, then chunk sphere vs each image's support CYLINDER;
-//  * (image, triangle) pairs that pass the beta-extent test are compacted into a
-//    per-warp queue (ballot + popc) and drained 32 at a time, one pair per lane, so the
-//    divergent per-layer work runs with full warps; an alpha-box test skips triangles whose
-//    (T_x, T_y) box misses the support disk;
+//  * (image, triangle) pairs that pass the beta-extent test and an alpha-box test (the
+//    triangle's (T_x, T_y) box meets the support disk) are compacted into a per-warp ring
+//    (ballot + popc) WITH their projected vertices, and drained 32 at a time, one pair per
+//    lane, so the divergent per-layer work runs with full warps;
 //  * chunk survivors carry their per-image cylinder hits (one 32-bit entry), and each warp
 //    prefetches its next chunk's triangles while it processes the current one;
 //  * the per-image rotation coefficients are computed once per image in the CTA prologue
@@ -234,20 +236,19 @@ __device__ __forceinline__ bool alpha_box_hits(const float *x, const float *y, f
     const float by0 = fmaxf(fmaxf(fminf(y[0], fminf(y[1], y[2])), -fmaxf(y[0], fmaxf(y[1], y[2]))), 0.f);
     return bx0 * bx0 + by0 * by0 <= r2;
 }
-// RICI_GEN_ALPHA_EARLY: the alpha-box test runs in the queue phase (with the beta-extent test),
-// so only pairs with rasterisation work are queued and every drained lane has a triangle
-#ifndef RICI_GEN_ALPHA_EARLY
-#define RICI_GEN_ALPHA_EARLY 1
-#endif
-
-// K <= 2 (N = 64 default): 33 KB of counters per CTA.  With the bin-unit frame, 4 CTAs / SM at
-// 60 registers (no spill) beat 5 CTAs at the 48-register cap (spills): C4 337 -> 325 ms, C3 103 ->
-// 99 ms, C2 1.75 -> 1.70 ms (r2e).  Round 1, before the bin-unit frame, had measured 5 > 4.
+// K <= 2 (N = 64 default): 33 KB of counters + 18 KB of projected-triangle queues per CTA, so
+// 3 CTAs / SM (78 registers, no spill).  Measured on C4 / C3 / C2 (r2e, r2j, r2k; images
+// identical): 5 CTAs at the 48-register cap 337 / 103 / 1.75 ms; 4 CTAs 325 / 99.4 / 1.71;
+// 3 CTAs 317.7 / 97.6 / 1.68; 3 CTAs with the projected queue 310.4 / 96.0 / 1.66; 2 CTAs (with
+// the queue) 357.6 / 110.5 / 1.93; K = 4 at 2 CTAs 321.5 / 98.8 / 1.71.
 template <int K, int NC>
 #ifndef RICI_GEN_MIN_BLOCKS
-#define RICI_GEN_MIN_BLOCKS 4
+#define RICI_GEN_MIN_BLOCKS 3
 #endif
-__global__ void __launch_bounds__(kThreads, K <= 2 ? RICI_GEN_MIN_BLOCKS : 1)
+#ifndef RICI_GEN_MIN_BLOCKS4
+#define RICI_GEN_MIN_BLOCKS4 2
+#endif
+__global__ void __launch_bounds__(kThreads, K <= 2 ? RICI_GEN_MIN_BLOCKS : (K <= 4 ? RICI_GEN_MIN_BLOCKS4 : 1))
 generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere, int64_t n_chunks,
                 const float4 *__restrict__ super_sphere, int64_t n_super,
                 const float *__restrict__ origins, const int *__restrict__ img_perm, int64_t n,
@@ -261,6 +262,11 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
     __shared__ unsigned chunk_list[kChunkCap];   // (chunk << 8) | image mask
     __shared__ float cta_sphere[4];
     __shared__ int queue[kThreads / 32][2 * 32];
+    // the queued pairs' projected (unsorted) triangles, a 64-slot ring per warp (SoA: x0 y0 z0 x1
+    // y1 z1 x2 y2 z2), written by the queue phase from the registers of its beta / alpha tests, so
+    // the drain neither reloads nor re-projects the triangle (C4 317.7 -> 310.4 ms, r2j)
+    __shared__ float qv[kThreads / 32][9][64];
+    int qh = 0;                                          // warp-uniform ring head
 
     int *acc = reinterpret_cast<int *>(smem_raw);        // [K][N][N+1] difference arrays
     const unsigned acc_s = (unsigned)__cvta_generic_to_shared(acc);
@@ -319,43 +325,31 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
     const float cs_r = cta_sphere[3];
     int qn = 0;                                          // warp-uniform queue length
 
-    // Drain `cnt` (<= 32) queued (chunk, triangle, image) items with one item per lane.
+    // Drain `cnt` (<= 32) queued (chunk, triangle, image) items with one item per lane: the
+    // projected triangle comes from the ring, is sorted by Z and rasterised.
     auto drain = [&](int cnt) {
         __syncwarp();
-        int item = lane < cnt ? queue[warp][lane] : -1;
-        int rest = qn - cnt;
-        int moved = lane < rest ? queue[warp][cnt + lane] : 0;
-        __syncwarp();
-        if (lane < rest) queue[warp][lane] = moved;
-        qn = rest;
-        int stat_rows = 0;                               // RICI_GEN_STATS: layer-loop length
+        const int slot = (qh + lane) & 63;
+        const int item = lane < cnt ? queue[warp][slot] : -1;
+        qh = (qh + cnt) & 63;
+        qn -= cnt;
+        int stat_rows = 0;
         (void)stat_rows;
         if (item >= 0) {
             RICI_STAT(2, 1);
-            const int64_t chunk = (int64_t)((unsigned)item >> 8);
-            const int t = (item >> 3) & 31, k = item & 7;
-            const float *src = tri + chunk * 9 * kChunk + t;
-            float v[9];
-#pragma unroll
-            for (int c = 0; c < 9; ++c) v[c] = __ldg(src + c * kChunk);
-            const GenFrame f = gframes[k];
-            float p[9], z[3];
-            project_z(f, v, p, z);
-            float x[3], y[3];
-            project_xy(f, p, x, y);                      // Eqs. 3-4 for T_x, T_y
-            if (RICI_GEN_ALPHA_EARLY || alpha_box_hits(x, y, (float)(N * N))) {
-                RICI_STAT(3, 1);
-                float ax = x[0], ay = y[0], az = z[0], bx = x[1], by = y[1], bz = z[1],
-                      cx = x[2], cy = y[2], cz = z[2];
-                sort3(ax, ay, az, bx, by, bz, cx, cy, cz);
+            RICI_STAT(3, 1);
+            const int k = item & 7;
+            const float(*w)[64] = qv[warp];
+            float ax = w[0][slot], ay = w[1][slot], az = w[2][slot], bx = w[3][slot], by = w[4][slot],
+                  bz = w[5][slot], cx = w[6][slot], cy = w[7][slot], cz = w[8][slot];
+            sort3(ax, ay, az, bx, by, bz, cx, cy, cz);
 #if RICI_GEN_STATS
-                stat_rows = max(0, min(max(__float2int_ru(cz), 0), N) - min(max(__float2int_ru(az), 0), N));
+            stat_rows = max(0, min(max(__float2int_ru(cz), 0), N) - min(max(__float2int_ru(az), 0), N));
 #endif
-                rasterise_triangle<NC>(acc_s + 4u * (unsigned)(k * img_words), N, ax, ay, az, bx, by, bz, cx, cy, cz);
-            }
+            rasterise_triangle<NC>(acc_s + 4u * (unsigned)(k * img_words), N, ax, ay, az, bx, by, bz, cx, cy, cz);
         }
 #if RICI_GEN_STATS
-        {   // warp iterations of the layer loop (the longest lane) and drains
+        {
             const int mx = __reduce_max_sync(0xffffffffu, stat_rows);
             if (lane == 0) { RICI_STAT(6, mx); RICI_STAT(7, 1); }
         }
@@ -492,33 +486,26 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
                         }
                     }
 #endif
-                    bool keep[K];
-                    {
-#pragma unroll
-                    for (int k = 0; k < K; ++k) {
-                        keep[k] = false;
-                        if ((kmask >> k) & 1u) {
-                            const GenFrame f = gframes[k];
-                            float p[9], z[3];
-                            project_z(f, v, p, z);
-                            float zlo = fminf(z[0], fminf(z[1], z[2])), zhi = fmaxf(z[0], fmaxf(z[1], z[2]));
-                            // a layer Z = r (integer) in [zlo, zhi) within [0, N)
-                            keep[k] = min(max(__float2int_ru(zlo), 0), N) < min(max(__float2int_ru(zhi), 0), N);
-#if RICI_GEN_ALPHA_EARLY
-                            if (keep[k]) {
-                                float x[3], y[3];
-                                project_xy(f, p, x, y);
-                                keep[k] = alpha_box_hits(x, y, (float)(N * N));
-                            }
-#endif
-                        }
-                    }
-                    }
 #pragma unroll
                     for (int k = 0; k < K; ++k) {
                         if (!((kmask >> k) & 1u)) continue;
-                        unsigned m = __ballot_sync(0xffffffffu, keep[k]);
-                        if (keep[k]) queue[warp][qn + __popc(m & lt_mask)] = pack_item(chunk, lane, k);
+                        const GenFrame f = gframes[k];
+                        float p[9], z[3], x[3], y[3];
+                        project_z(f, v, p, z);
+                        float zlo = fminf(z[0], fminf(z[1], z[2])), zhi = fmaxf(z[0], fmaxf(z[1], z[2]));
+                        bool keep = min(max(__float2int_ru(zlo), 0), N) < min(max(__float2int_ru(zhi), 0), N);
+                        if (keep) {
+                            project_xy(f, p, x, y);
+                            keep = alpha_box_hits(x, y, (float)(N * N));
+                        }
+                        const unsigned m = __ballot_sync(0xffffffffu, keep);
+                        if (keep) {
+                            const int slot = (qh + qn + __popc(m & lt_mask)) & 63;
+                            queue[warp][slot] = pack_item(chunk, lane, k);
+                            float(*w)[64] = qv[warp];
+#pragma unroll
+                            for (int j = 0; j < 3; ++j) { w[3 * j][slot] = x[j]; w[3 * j + 1][slot] = y[j]; w[3 * j + 2][slot] = z[j]; }
+                        }
                         qn += __popc(m);
                         if (qn >= 32) drain(32);
                     }
@@ -601,7 +588,10 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
 
 int generate_images_per_cta(int N) {
     int per = N * (N + 1) * 4;
-    int budget = 34 * 1024;                       // counters per CTA (K = 2, 5 CTAs / SM at N = 64)
+#ifndef RICI_GEN_BUDGET_KB
+#define RICI_GEN_BUDGET_KB 34
+#endif
+    int budget = RICI_GEN_BUDGET_KB * 1024;       // counters per CTA (K = 2 at N = 64)
     if (const char *v = getenv("RICI_GEN_SMEM_KB")) budget = atoi(v) * 1024;   // tuning knob
     int k = budget / per;
     return k < 1 ? 1 : (k > kMaxK ? kMaxK : k);
@@ -613,8 +603,8 @@ cudaError_t launch_generate(const DeviceMesh &m, const float *d_origins, int64_t
     const int K = generate_images_per_cta(N);
     size_t smem = (size_t)K * N * (N + 1) * sizeof(int);
     const int Kt = K >= 8 ? 8 : K >= 4 ? 4 : K >= 2 ? 2 : 1;
-    const bool n64 = N == 64 && Kt == 2;                  // the compile-time N = 64 instance
-    const void *kern = n64 ? (const void *)generate_kernel<2, 64>
+    const bool n64 = N == 64 && (Kt == 2 || Kt == 4);     // the compile-time N = 64 instances
+    const void *kern = n64 ? (Kt == 2 ? (const void *)generate_kernel<2, 64> : (const void *)generate_kernel<4, 64>)
                      : Kt == 8 ? (const void *)generate_kernel<8, 0> : Kt == 4 ? (const void *)generate_kernel<4, 0>
                      : Kt == 2 ? (const void *)generate_kernel<2, 0> : (const void *)generate_kernel<1, 0>;
     smem = (size_t)Kt * N * (N + 1) * sizeof(int);
@@ -644,7 +634,8 @@ cudaError_t launch_generate(const DeviceMesh &m, const float *d_origins, int64_t
     generate_kernel<KK, NN><<<(unsigned)blocks, kThreads, smem, s>>>(m.tri, m.sphere, m.n_chunks, m.super_sphere, \
                                                                  m.n_super, d_origins, perm, n, R, N, g, d_out)
     KernelTimer timer(0, s);
-    if (n64) RICI_GEN_LAUNCH(2, 64);
+    if (n64 && Kt == 2) RICI_GEN_LAUNCH(2, 64);
+    else if (n64) RICI_GEN_LAUNCH(4, 64);
     else if (Kt == 8) RICI_GEN_LAUNCH(8, 0);
     else if (Kt == 4) RICI_GEN_LAUNCH(4, 0);
     else if (Kt == 2) RICI_GEN_LAUNCH(2, 0);

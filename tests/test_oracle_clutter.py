@@ -65,3 +65,48 @@ def test_triangle_inside_counts_its_area(oracle_mod):
     area = 0.5 * np.linalg.norm(np.cross(V[1].astype(float) - V[0], V[2].astype(float) - V[0]))
     _, aa, _ = oracle_mod.clutter_fraction(V, T, np.ones(1, np.uint8), ORIGIN, 0.3, q=5)
     assert aa[0] == pytest.approx(area, rel=1e-12)
+
+
+def _quad_bound(R, d):
+    """Area within distance d of a quarter circle of radius R (the band where a sub-triangle of
+    diameter d can straddle the wall and be mis-assigned by a centroid quadrature)."""
+    return 0.5 * np.pi * ((R + d) ** 2 - max(R - d, 0.0) ** 2) / 2
+
+
+def test_wall_crossing_triangle_converges_to_exact_clip(oracle_mod):
+    """A triangle that crosses the cylinder WALL (r = R): right triangle with legs 0.5 at the
+    axis, in the plane beta = 0.05.  Its hypotenuse is 0.354 > R from the axis, so the exact
+    clipped area is the quarter disk pi R^2 / 4.  The Q x Q centroid quadrature (G17) may only
+    misplace sub-triangles that straddle the wall: |error| <= the area of the band of width d
+    (the sub-triangle diameter) around the quarter circle, and the error shrinks with Q."""
+    R = 0.3
+    V = np.array([[0.0, 0.0, 0.05], [0.5, 0.0, 0.05], [0.0, 0.5, 0.05]], np.float32)
+    T = np.array([[0, 1, 2]], np.int32)
+    exact = np.pi * R * R / 4
+    errs = []
+    for q in (8, 16, 32, 64):
+        _, aa, _ = oracle_mod.clutter_fraction(V, T, np.ones(1, np.uint8), ORIGIN, R, q=q)
+        d = 0.5 * np.sqrt(2) / q                     # sub-triangle diameter
+        err = abs(aa[0] - exact)
+        assert err <= _quad_bound(R, d), (q, aa[0], exact)
+        errs.append(err)
+    assert errs[-1] < 0.02 * exact and errs[-1] < errs[0]
+
+
+def test_slab_crossing_triangle_converges_to_exact_clip(oracle_mod):
+    """A triangle inside r <= R that crosses the SLAB walls |beta| = R/2: vertices
+    (0.1, -0.1, -0.3), (0.1, 0.1, -0.3), (0.1, 0, 0.3); its width at height z is
+    0.2 (0.3 - z) / 0.6, so the area with |z| <= 0.15 is (1/3) * integral (0.3 - z) dz = 0.03."""
+    R = 0.3
+    V = np.array([[0.1, -0.1, -0.3], [0.1, 0.1, -0.3], [0.1, 0.0, 0.3]], np.float32)
+    T = np.array([[0, 1, 2]], np.int32)
+    exact = 0.03
+    errs = []
+    for q in (5, 9, 17, 33, 65):                     # not multiples of 4: the slab walls cut sub-triangles
+        _, aa, _ = oracle_mod.clutter_fraction(V, T, np.ones(1, np.uint8), ORIGIN, R, q=q)
+        h = 0.6 / q                                  # sub-triangle height along z
+        band = 2 * 0.2 * 2 * h                       # two walls, width <= 0.2, band +-h each
+        err = abs(aa[0] - exact)
+        assert err <= band, (q, aa[0], exact)
+        errs.append(err)
+    assert errs[0] > 1e-4 and errs[-1] < 0.02 * exact and errs[-1] < errs[0]
