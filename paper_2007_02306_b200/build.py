@@ -32,6 +32,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for src in SOURCES:
         obj = os.path.join(CSRC, src.replace(".cu", ".o"))
         extra = ["-ftz=true"] if src in ("generate.cu", "clutter.cu") else []     # denormals cannot matter at 1e-5*R
+        if src == "generate.cu":        # no FMA contraction: the arithmetic is exactly the source's fmaf / FFMA2
+            extra += ["-fmad=false"]    # (otherwise inlining context decides which a*b+c fuse: C3 tie pixels moved)
         cmd = [NVCC, *FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:

@@ -419,73 +419,52 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
                 // Level 3: static round-robin over the warps, so each warp knows its next chunk
                 // and prefetches its nine triangle planes while the current one is processed
                 // (measured faster than a shared-counter schedule with the same prefetch).
-                int e = warp;
-                unsigned nxt_ent = 0;
-                float nv9[9];
-                if (e < n_ck) {
-                    nxt_ent = chunk_list[e];
-                    const float *src = tri + (int64_t)(nxt_ent >> 8) * 9 * kChunk + lane;
-#pragma unroll
-                    for (int c = 0; c < 9; ++c) nv9[c] = __ldg(src + c * kChunk);
-                }
-                while (e < n_ck) {
-                    const unsigned ent = nxt_ent;
+                // each chunk: its (image, triangle) pairs -- beta-extent test: does a
+                // layer Z = r lie in [z_min, z_max)?  then the alpha box; survivors go to the
+                // warp's ring with their projected vertices
+                auto process = [&](const unsigned ent, const float *v) {
                     const int64_t chunk = (int64_t)(ent >> 8);
                     const unsigned kmask = ent & 0xffu;
                     if (lane == 0) { RICI_STAT(0, 1); RICI_STAT(1, __popc(kmask)); }
-                    float v[9];
-#pragma unroll
-                    for (int c = 0; c < 9; ++c) v[c] = nv9[c];
-                    e += kThreads / 32;
-                    if (e < n_ck) {
-                        nxt_ent = chunk_list[e];
-                        const float *src = tri + (int64_t)(nxt_ent >> 8) * 9 * kChunk + lane;
-#pragma unroll
-                        for (int c = 0; c < 9; ++c) nv9[c] = __ldg(src + c * kChunk);
-                    }
-                    // (image, triangle) pairs -- beta-extent test: does a layer centre
-                    // lie in [z_min, z_max)?  Survivors go to the warp's queue.
-                    // the K images' tests are independent chains: computed together (ILP), then
-                    // pushed in image order
-#if RICI_GEN_STATS
-                    {   // finer culls, counted only: the 8-triangle sub-chunk's sphere and the triangle's
-                        // own sphere against each tested image's support cylinder (stats 10, 11)
-                        float tc[3], tr = 0.f;
-                        for (int a = 0; a < 3; ++a) tc[a] = (v[a] + v[3 + a] + v[6 + a]) * (1.f / 3.f);
-                        for (int j = 0; j < 3; ++j) {
-                            float dx = v[3 * j] - tc[0], dy = v[3 * j + 1] - tc[1], dz = v[3 * j + 2] - tc[2];
-                            tr = fmaxf(tr, sqrtf(dx * dx + dy * dy + dz * dz));
-                        }
-                        float lo[3], hi[3];
-                        for (int a = 0; a < 3; ++a) { lo[a] = tc[a] - tr; hi[a] = tc[a] + tr; }
-                        for (int o = 1; o < 8; o <<= 1)
-                            for (int a = 0; a < 3; ++a) {
-                                lo[a] = fminf(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
-                                hi[a] = fmaxf(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+    #if RICI_GEN_STATS
+                        {   // finer culls, counted only: the 8-triangle sub-chunk's sphere and the triangle's
+                            // own sphere against each tested image's support cylinder (stats 10, 11)
+                            float tc[3], tr = 0.f;
+                            for (int a = 0; a < 3; ++a) tc[a] = (v[a] + v[3 + a] + v[6 + a]) * (1.f / 3.f);
+                            for (int j = 0; j < 3; ++j) {
+                                float dx = v[3 * j] - tc[0], dy = v[3 * j + 1] - tc[1], dz = v[3 * j + 2] - tc[2];
+                                tr = fmaxf(tr, sqrtf(dx * dx + dy * dy + dz * dz));
                             }
-                        float sc[3], sr = 0.f;
-                        for (int a = 0; a < 3; ++a) sc[a] = 0.5f * (lo[a] + hi[a]);
-                        {
-                            float dx = tc[0] - sc[0], dy = tc[1] - sc[1], dz = tc[2] - sc[2];
-                            sr = sqrtf(dx * dx + dy * dy + dz * dz) + tr;
+                            float lo[3], hi[3];
+                            for (int a = 0; a < 3; ++a) { lo[a] = tc[a] - tr; hi[a] = tc[a] + tr; }
+                            for (int o = 1; o < 8; o <<= 1)
+                                for (int a = 0; a < 3; ++a) {
+                                    lo[a] = fminf(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+                                    hi[a] = fmaxf(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+                                }
+                            float sc[3], sr = 0.f;
+                            for (int a = 0; a < 3; ++a) sc[a] = 0.5f * (lo[a] + hi[a]);
+                            {
+                                float dx = tc[0] - sc[0], dy = tc[1] - sc[1], dz = tc[2] - sc[2];
+                                sr = sqrtf(dx * dx + dy * dy + dz * dz) + tr;
+                            }
+                            for (int o = 1; o < 8; o <<= 1) sr = fmaxf(sr, __shfl_xor_sync(0xffffffffu, sr, o));
+                            for (int k = 0; k < K; ++k) {
+                                if (!((kmask >> k) & 1u)) continue;
+                                const Frame &f = frames[k];
+                                auto cyl = [&](const float *c, float w) {
+                                    const float pad = 1e-4f * R + 1e-6f * (fabsf(c[0]) + fabsf(c[1]) + fabsf(c[2]) + w);
+                                    const float ra = R + w + pad, hb = 0.5f * R + w + pad;
+                                    float ex = c[0] - f.sx, ey = c[1] - f.sy, ez = c[2] - f.sz;
+                                    float b = fmaf(f.czx, ex, fmaf(f.czy, ey, f.czz * ez));
+                                    float a2 = fmaxf(ex * ex + ey * ey + ez * ez - b * b, 0.f);
+                                    return fabsf(b) <= hb && a2 <= ra * ra;
+                                };
+                                RICI_STAT(10, cyl(sc, sr) ? 1 : 0);
+                                RICI_STAT(11, cyl(tc, tr) ? 1 : 0);
+                            }
                         }
-                        for (int o = 1; o < 8; o <<= 1) sr = fmaxf(sr, __shfl_xor_sync(0xffffffffu, sr, o));
-                        for (int k = 0; k < K; ++k) {
-                            if (!((kmask >> k) & 1u)) continue;
-                            const Frame &f = frames[k];
-                            auto cyl = [&](const float *c, float w) {
-                                const float pad = 1e-4f * R + 1e-6f * (fabsf(c[0]) + fabsf(c[1]) + fabsf(c[2]) + w);
-                                const float ra = R + w + pad, hb = 0.5f * R + w + pad;
-                                float ex = c[0] - f.sx, ey = c[1] - f.sy, ez = c[2] - f.sz;
-                                float b = fmaf(f.czx, ex, fmaf(f.czy, ey, f.czz * ez));
-                                float a2 = fmaxf(ex * ex + ey * ey + ez * ez - b * b, 0.f);
-                                return fabsf(b) <= hb && a2 <= ra * ra;
-                            };
-                            RICI_STAT(10, cyl(sc, sr) ? 1 : 0);
-                            RICI_STAT(11, cyl(tc, tr) ? 1 : 0);
-                        }
-                    }
-#endif
+    #endif
 #pragma unroll
                     for (int k = 0; k < K; ++k) {
                         if (!((kmask >> k) & 1u)) continue;
@@ -502,12 +481,38 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
                         if (keep) {
                             const int slot = (qh + qn + __popc(m & lt_mask)) & 63;
                             queue[warp][slot] = pack_item(chunk, lane, k);
-                            float(*w)[64] = qv[warp];
+                            float *w = &qv[warp][0][slot];
 #pragma unroll
-                            for (int j = 0; j < 3; ++j) { w[3 * j][slot] = x[j]; w[3 * j + 1][slot] = y[j]; w[3 * j + 2][slot] = z[j]; }
+                            for (int j = 0; j < 3; ++j) { w[(3 * j) * 64] = x[j]; w[(3 * j + 1) * 64] = y[j]; w[(3 * j + 2) * 64] = z[j]; }
                         }
                         qn += __popc(m);
                         if (qn >= 32) drain(32);
+                    }
+                };
+                // static round-robin over the warps, so each warp knows its next chunk and
+                // prefetches its nine triangle planes while the current one is processed
+                // (measured faster than a shared-counter schedule with the same prefetch)
+                auto load = [&](int e, float *v) -> unsigned {
+                    const unsigned ent = chunk_list[e];
+                    const float *src = tri + (int64_t)(ent >> 8) * 9 * kChunk + lane;
+#pragma unroll
+                    for (int c = 0; c < 9; ++c) v[c] = __ldg(src + c * kChunk);
+                    return ent;
+                };
+                constexpr int kW = kThreads / 32;
+                {
+                    float nv9[9];
+                    unsigned nxt_ent = 0;
+                    int e = warp;
+                    if (e < n_ck) nxt_ent = load(e, nv9);
+                    while (e < n_ck) {
+                        const unsigned ent = nxt_ent;
+                        float v[9];
+#pragma unroll
+                        for (int c = 0; c < 9; ++c) v[c] = nv9[c];
+                        e += kW;
+                        if (e < n_ck) nxt_ent = load(e, nv9);
+                        process(ent, v);
                     }
                 }
                 __syncthreads();
