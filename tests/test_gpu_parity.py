@@ -406,8 +406,9 @@ def test_rank_mode_tensor_pruning_exact(rici, oracle_mod, seed):
 def test_crss_paths_agree_subprocess(tmp_path):
     """The SIMT path (RICI_CRSS_PATH=simt) and the four tensor-core kernels (RICI_MMA_MODE 0:
     1-CTA, 1: 2-CTA multicast, 2: cta_group::2, 3: cta_group::2 with 2:4-sparse needle rows, one
-    or two haystack tiles per staged needle block, RICI_SP_NT, with and without a haystack slice
-    on the SMs the 4-CTA clusters leave free, RICI_SP_SIDE_FRAC) give identical ranks and counts, in
+    or two haystack tiles per staged needle block, RICI_SP_NT, or two needle m tiles per staged
+    haystack block, RICI_SP_2M, with and without a haystack slice on the SMs the 4-CTA clusters
+    leave free, RICI_SP_SIDE_FRAC) give identical ranks and counts, in
     full mode and in rank mode (early exit: tile pruning on K prefixes)."""
     import os
     import subprocess
@@ -428,15 +429,18 @@ def test_crss_paths_agree_subprocess(tmp_path):
         "early = r.rici_crss_search(nee, im, early_exit=True).cpu().numpy()\n"
         "np.save(sys.argv[1], np.concatenate([ranks.astype(np.int64), cnt.astype(np.int64), early.astype(np.int64)]))\n") % root
     outs = {}
-    for path, mode, nt, side in (("simt", "2", "2", "0"), ("mma", "0", "2", "0"), ("mma", "1", "2", "0"),
-                                 ("mma", "2", "2", "0"), ("mma", "3", "1", "0"), ("mma", "3", "2", "0"),
-                                 ("mma", "3", "1", "0.3"), ("mma", "3", "2", "0.3")):
-        env = dict(os.environ, RICI_CRSS_PATH=path, RICI_MMA_MODE=mode, RICI_SP_NT=nt, RICI_SP_SIDE_FRAC=side)
-        key = f"{path}{mode}_{nt}_{side}"
+    for path, mode, nt, side, two_m in (("simt", "2", "2", "0", "0"), ("mma", "0", "2", "0", "0"),
+                                        ("mma", "1", "2", "0", "0"), ("mma", "2", "2", "0", "0"),
+                                        ("mma", "3", "1", "0", "0"), ("mma", "3", "2", "0", "0"),
+                                        ("mma", "3", "1", "0.3", "0"), ("mma", "3", "2", "0.3", "0"),
+                                        ("mma", "3", "2", "0", "1"), ("mma", "3", "2", "0.3", "1")):
+        env = dict(os.environ, RICI_CRSS_PATH=path, RICI_MMA_MODE=mode, RICI_SP_NT=nt, RICI_SP_SIDE_FRAC=side,
+                   RICI_SP_2M=two_m)   # RICI_SP_2M: two m tiles per sparse unit (kNM = 2)
+        key = f"{path}{mode}_{nt}_{side}_{two_m}"
         f = str(tmp_path / f"{key}.npy")
         subprocess.run([sys.executable, "-c", code, f], env=env, check=True, timeout=600)
         outs[key] = np.load(f)
-    ref = outs.pop("simt2_2_0")
+    ref = outs.pop("simt2_2_0_0")
     assert ref[:2000].max() > 0 and ref[2000:4000].max() > 0  # ranks and counts not trivially zero
     assert np.array_equal(ref[:2000], ref[4000:])            # rank mode (early exit) = full mode
     for k, v in outs.items():
