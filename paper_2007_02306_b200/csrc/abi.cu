@@ -318,7 +318,7 @@ rici_status rici_create_mesh(const float *vertices, int64_t n_vertices, const in
     cudaError_t e = cudaSuccess;
     if (n_chunks > 0) {
         // stream-ordered pool allocations: no device-wide synchronisation on create/destroy
-        e = cudaMallocAsync((void **)&mesh->m.tri, sizeof(float) * 9 * rici::kChunk * (size_t)n_chunks, s);
+        e = cudaMallocAsync((void **)&mesh->m.tri, sizeof(float) * rici::kTriFloatsPerChunk * (size_t)n_chunks, s);
         if (e == cudaSuccess) e = cudaMallocAsync((void **)&mesh->m.sphere, sizeof(float4) * (size_t)n_chunks, s);
         if (e == cudaSuccess)
             e = cudaMallocAsync((void **)&mesh->m.super_sphere,

@@ -59,10 +59,8 @@ clutter_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere,
                     cm &= cm - 1;
                     const int64_t slot = chunk * kChunk + lane;
                     if (slot >= nt) continue;               // padding of the last chunk
-                    const float *src = tri + chunk * 9 * kChunk + lane;
                     float v[9];
-#pragma unroll
-                    for (int c = 0; c < 9; ++c) v[c] = __ldg(src + c * kChunk);
+                    load_triangle(tri, chunk, lane, v);
                     const float e1x = v[3] - v[0], e1y = v[4] - v[1], e1z = v[5] - v[2];
                     const float e2x = v[6] - v[0], e2y = v[7] - v[1], e2z = v[8] - v[2];
                     const float cx = e1y * e2z - e1z * e2y, cy = e1z * e2x - e1x * e2z, cz = e1x * e2y - e1y * e2x;

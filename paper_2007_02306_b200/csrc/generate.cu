@@ -57,6 +57,7 @@ constexpr int kChunkCap = 1024;          // chunk survivors per batch (multiple 
 // cvt.rpi.s32.f32 (__float2int_ru) is ceil with saturation (NaN -> 0).  Exact ties are fragile
 // pixels (G5).
 
+// Stable sort of three vertices by z (a three-stage network; equal z keep their order).
 __device__ __forceinline__ void sort3(float &ax, float &ay, float &az, float &bx, float &by,
                                       float &bz, float &cx, float &cy, float &cz) {
 #define RICI_SWAP(p, q) { float t = p; p = q; q = t; }
@@ -194,38 +195,42 @@ __device__ __forceinline__ void rasterise_triangle(unsigned acc, int n_rt,
 // The per-image projection in bin units: translation first (Eq. 2, S_v), then the composed
 // rotation of Eqs. 3-4 scaled by 1/delta, with the row offset folded into Z.
 struct __align__(16) GenFrame {
-    float sx, sy, sz, zoff;      // S_v; N/2 - 1/2
+    float nsx, nsy, nsz, zoff;   // -S_v (p = v + (-S_v) is bitwise v - S_v); N/2 - 1/2
     float xx, xy, xz, yx;        // X = xx px + xy py + xz pz;  Y = yx px + yy py
     float yy, zx, zy, zz;        // Z = zx px + zy py + zz pz + zoff
 };
 __device__ __forceinline__ GenFrame gen_frame(const Frame &f, float inv_delta, float zoff) {
     GenFrame q;
-    q.sx = f.sx; q.sy = f.sy; q.sz = f.sz; q.zoff = zoff;
+    q.nsx = -f.sx; q.nsy = -f.sy; q.nsz = -f.sz; q.zoff = zoff;
     q.xx = f.nbz * f.nax * inv_delta; q.xy = f.nbz * f.nay * inv_delta; q.xz = -f.nbx * inv_delta;
     q.yx = -f.nay * inv_delta; q.yy = f.nax * inv_delta;
     q.zx = f.czx * inv_delta; q.zy = f.czy * inv_delta; q.zz = f.czz * inv_delta;
     return q;
 }
 
-// Project one triangle into image k's spin frame (Eqs. 2-4); the same arithmetic decides the
-// cull (in the queue phase) and the rasterisation, so the two can never disagree.
-__device__ __forceinline__ void project_z(const GenFrame &f, const float *v, float *p, float *z) {
-#pragma unroll
-    for (int j = 0; j < 3; ++j) {
-        p[3 * j] = v[3 * j] - f.sx;                     // Eq. 2: translate first
-        p[3 * j + 1] = v[3 * j + 1] - f.sy;
-        p[3 * j + 2] = v[3 * j + 2] - f.sz;
-        z[j] = fmaf(f.zx, p[3 * j], fmaf(f.zy, p[3 * j + 1], fmaf(f.zz, p[3 * j + 2], f.zoff)));   // T_z
-    }
+// Project one triangle into image k's spin frame (Eqs. 2-4): translate first (Eq. 2), then the
+// scaled rotation.  Vertices 0 and 1 go through packed FP32x2 (FADD2 / FFMA2 / FMUL2, the frame
+// coefficient broadcast), vertex 2 through the scalar ops: every lane of a packed op is the
+// scalar operation in the same order, so a shared vertex projects bitwise alike in every
+// triangle (C4 289.4 -> 283 ms with the float beta test below, r2y).  pp = translated vertices
+// 0 and 1 (x, y, z pairs), p2 = translated vertex 2.
+__device__ __forceinline__ void project_z(const GenFrame &f, const float *v, float2 *pp, float *p2, float *z) {
+    pp[0] = __fadd2_rn(f2(v[0], v[3]), f2(f.nsx, f.nsx));
+    pp[1] = __fadd2_rn(f2(v[1], v[4]), f2(f.nsy, f.nsy));
+    pp[2] = __fadd2_rn(f2(v[2], v[5]), f2(f.nsz, f.nsz));
+    p2[0] = v[6] + f.nsx; p2[1] = v[7] + f.nsy; p2[2] = v[8] + f.nsz;
+    const float2 z01 = __ffma2_rn(f2(f.zx, f.zx), pp[0],
+                                  __ffma2_rn(f2(f.zy, f.zy), pp[1], __ffma2_rn(f2(f.zz, f.zz), pp[2], f2(f.zoff, f.zoff))));
+    z[0] = z01.x; z[1] = z01.y;
+    z[2] = fmaf(f.zx, p2[0], fmaf(f.zy, p2[1], fmaf(f.zz, p2[2], f.zoff)));
 }
-
-// Eqs. 3-4 for T_x, T_y of the three translated vertices p (project_z output).
-__device__ __forceinline__ void project_xy(const GenFrame &f, const float *p, float *x, float *y) {
-#pragma unroll
-    for (int j = 0; j < 3; ++j) {
-        y[j] = fmaf(f.yx, p[3 * j], f.yy * p[3 * j + 1]);
-        x[j] = fmaf(f.xx, p[3 * j], fmaf(f.xy, p[3 * j + 1], f.xz * p[3 * j + 2]));
-    }
+// Eqs. 3-4 for T_x, T_y of the translated vertices (project_z output).
+__device__ __forceinline__ void project_xy(const GenFrame &f, const float2 *pp, const float *p2, float *x, float *y) {
+    const float2 y01 = __ffma2_rn(f2(f.yx, f.yx), pp[0], __fmul2_rn(f2(f.yy, f.yy), pp[1]));
+    const float2 x01 = __ffma2_rn(f2(f.xx, f.xx), pp[0], __ffma2_rn(f2(f.xy, f.xy), pp[1], __fmul2_rn(f2(f.xz, f.xz), pp[2])));
+    y[0] = y01.x; y[1] = y01.y; x[0] = x01.x; x[1] = x01.y;
+    y[2] = fmaf(f.yx, p2[0], f.yy * p2[1]);
+    x[2] = fmaf(f.xx, p2[0], fmaf(f.xy, p2[1], f.xz * p2[2]));
 }
 // alpha cull: if the triangle's (T_x, T_y) bounding box misses the support disk (radius N in
 // bin units), every slice point has alpha > R > rho_{N-1} and no bin can be hit (exact skip)
@@ -466,12 +471,17 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
                     for (int k = 0; k < K; ++k) {
                         if (!((kmask >> k) & 1u)) continue;
                         const GenFrame f = gframes[k];
-                        float p[9], z[3], x[3], y[3];
-                        project_z(f, v, p, z);
+                        float z[3], x[3], y[3];
+                        float2 pp[3];
+                        float p2[3];
+                        project_z(f, v, pp, p2, z);
                         float zlo = fminf(z[0], fminf(z[1], z[2])), zhi = fmaxf(z[0], fmaxf(z[1], z[2]));
-                        bool keep = min(max(__float2int_ru(zlo), 0), N) < min(max(__float2int_ru(zhi), 0), N);
+                        // beta-extent test: a layer Z = r in [zlo, zhi) with 0 <= r < N,
+                        // i.e. the first row at or above max(zlo, 0) lies below min(zhi, N)
+                        // (one FRND.CEIL; C4 289.4 -> 286.4 ms against ceil-to-int and clamps, r2x)
+                        bool keep = ceilf(fmaxf(zlo, 0.f)) < fminf(zhi, (float)N);
                         if (keep) {
-                            project_xy(f, p, x, y);
+                            project_xy(f, pp, p2, x, y);
                             keep = alpha_box_hits(x, y, (float)(N * N));
                         }
                         const unsigned m = __ballot_sync(0xffffffffu, keep);
@@ -490,9 +500,7 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
                 // (measured faster than a shared-counter schedule with the same prefetch)
                 auto load = [&](int e, float *v) -> unsigned {
                     const unsigned ent = chunk_list[e];
-                    const float *src = tri + (int64_t)(ent >> 8) * 9 * kChunk + lane;
-#pragma unroll
-                    for (int c = 0; c < 9; ++c) v[c] = __ldg(src + c * kChunk);
+                    load_triangle(tri, (int64_t)(ent >> 8), lane, v);
                     return ent;
                 };
                 constexpr int kW = kThreads / 32;

@@ -1,0 +1,3 @@
+set -x
+MODE=gen ROUNDS=2 REPS=3 WORKLOADS=c2,c3,c4 timeout 1500 python scripts/variant_time.py scratch/g_base scratch/g_triaos > gpurun_out/r2v_gen_variants.jsonl 2>&1; echo sweep rc=$?
+cat gpurun_out/r2v_gen_variants.jsonl
