@@ -317,6 +317,24 @@ def test_crss_count_mma_guard_and_fallback(rici, oracle_mod, big):
     assert np.array_equal(r.astype(np.uint32), oracle_mod.ranks(A, H))
 
 
+def test_guard_fallback_many_haystack_images(rici, oracle_mod):
+    """The haystack-side guard fallback keeps at most 20 guard-breaking haystack images resident
+    per pass: 47 of them (three passes) against needles whose change lists overflow the
+    512-entry per-warp list several times (density 0.3 -> ~2,000 changes per needle); counts and
+    ranks must equal the oracle exactly."""
+    rng = np.random.default_rng(2024)
+    A = _mixed_images(rng, 260, 9, 3, 300)
+    H = np.concatenate([A, _mixed_images(rng, 400, 9, 47, 40)])
+    dh = np.abs(np.diff(H.astype(np.int64), axis=2)).reshape(H.shape[0], -1).max(1)
+    assert int((dh > 15).sum()) >= 47
+    D = oracle_mod.crss_matrix(A, H)
+    thr = D[np.arange(260), rng.integers(0, H.shape[0], 260)].copy()
+    got = rici.rici_crss_count_below(_dev(A), _dev(H), torch.from_numpy(thr.view(np.int64)).to(DEV))
+    assert np.array_equal(got.cpu().numpy().astype(np.int64), (D < thr[:, None]).sum(1))
+    r = rici.rici_crss_search(_dev(A), _dev(H)).cpu().numpy()
+    assert np.array_equal(r.astype(np.uint32), oracle_mod.ranks(A, H))
+
+
 def test_search_captured_in_cuda_graph(rici, oracle_mod):
     """No host synchronisation anywhere in rici_crss_search / count_below (tensor path with the
     device-sized dense subset and guard fallback): the calls capture into a CUDA graph, and the
