@@ -23,5 +23,6 @@ rici.rici_crss_search(imgs[0], imgs[1]); lib.rici_debug_sp_prof(buf, 1)
 rici.rici_crss_search(imgs[0], imgs[1]); torch.cuda.synchronize(); lib.rici_debug_sp_prof(buf, 1)
 v = list(buf)
 print(json.dumps({"producer_wait_empty": v[0], "mma_wait_full": v[1], "mma_wait_epilogue": v[2],
-                  "mma_issuer_total": v[3], "stages": v[4],
+                  "mma_issuer_total": v[3], "stages": v[4], "drain_cycles_mean": v[5] / max(v[6], 1),
+                  "cycles_per_unit": v[3] / max(v[4], 1) * 32 if v[4] else None,
                   "frac_wait_full": v[1] / max(v[3], 1), "frac_wait_epilogue": v[2] / max(v[3], 1)}))
