@@ -1,22 +1,33 @@
 """Kernel timeline of one C2 step (create_mesh + generate + search) from the torch profiler
-(CUPTI activity records: start/end of every kernel on every stream) -- finds gaps and overlap."""
+(CUPTI activity records: start/end of every kernel on every stream) -- finds gaps and overlap.
+WORKLOAD=c4: only the C4 search (images generated first, outside the profile)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from torch.profiler import profile, ProfilerActivity
 import synth, paper_2007_02306_b200 as rici
 
-cfg = synth.config_c2(); m = cfg["mesh"]
-v, t, o = (torch.from_numpy(x).cuda() for x in (m.vertices, m.indices, cfg["origins"]))
-imgs = torch.empty((len(cfg["origins"]), 64, 64), dtype=torch.int16, device="cuda")
-ranks = torch.empty(len(cfg["origins"]), dtype=torch.int32, device="cuda")
+if os.environ.get("WORKLOAD") == "c4":
+    c4 = synth.config_c4()
+    gen = []
+    for mm in (c4["reference"], c4["scene"]):
+        mesh = rici.rici_create_mesh(torch.from_numpy(mm.vertices).cuda(), torch.from_numpy(mm.indices).cuda())
+        gen.append(rici.rici_generate(mesh, torch.from_numpy(mm.origins).cuda(), 0.3, 64))
+    ranks = torch.empty(gen[0].shape[0], dtype=torch.int32, device="cuda")
 
+    def step():
+        rici.rici_crss_search(gen[0], gen[1], out=ranks)
+else:
+    cfg = synth.config_c2(); m = cfg["mesh"]
+    v, t, o = (torch.from_numpy(x).cuda() for x in (m.vertices, m.indices, cfg["origins"]))
+    imgs = torch.empty((len(cfg["origins"]), 64, 64), dtype=torch.int16, device="cuda")
+    ranks = torch.empty(len(cfg["origins"]), dtype=torch.int32, device="cuda")
 
-def step():
-    mesh = rici.rici_create_mesh(v, t)
-    rici.rici_generate(mesh, o, 0.3, 64, out=imgs)
-    rici.rici_crss_search(imgs, imgs, out=ranks)
-    mesh.destroy()
+    def step():
+        mesh = rici.rici_create_mesh(v, t)
+        rici.rici_generate(mesh, o, 0.3, 64, out=imgs)
+        rici.rici_crss_search(imgs, imgs, out=ranks)
+        mesh.destroy()
 
 
 for _ in range(3):
