@@ -7,7 +7,19 @@ import torch
 from torch.profiler import profile, ProfilerActivity
 import synth, paper_2007_02306_b200 as rici
 
-if os.environ.get("WORKLOAD") == "c4":
+if os.environ.get("WORKLOAD") == "c4step":          # the whole bench step (bench.py, N = 1)
+    c4 = synth.config_c4()
+    dev = [[torch.from_numpy(x).cuda() for x in (mm.vertices, mm.indices, mm.origins)] for mm in (c4["reference"], c4["scene"])]
+    outs = [torch.empty((d[2].shape[0], 64, 64), dtype=torch.int16, device="cuda") for d in dev]
+    ranks = torch.empty(outs[0].shape[0], dtype=torch.int32, device="cuda")
+
+    def step():
+        for d, o in zip(dev, outs):
+            mesh = rici.rici_create_mesh(d[0], d[1])
+            rici.rici_generate(mesh, d[2], 0.3, 64, out=o)
+            mesh.destroy()
+        rici.rici_crss_search(outs[0], outs[1], out=ranks)
+elif os.environ.get("WORKLOAD") == "c4":
     c4 = synth.config_c4()
     gen = []
     for mm in (c4["reference"], c4["scene"]):
