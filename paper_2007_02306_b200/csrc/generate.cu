@@ -28,10 +28,12 @@
 //    lane, so the divergent per-layer work runs with full warps;
 //  * chunk survivors carry their per-image cylinder hits (one 32-bit entry), and each warp
 //    prefetches its next chunk's triangles while it processes the current one;
+//  * no FMA contraction (-fmad=false, build.py): every fused multiply-add is an explicit fmaf /
+//    FFMA2, so the arithmetic (and every tie decision) is exactly the source's;
 //  * the per-image rotation coefficients are computed once per image in the CTA prologue
 //    ("out of the inner loop");
 //  * saturation to uint16 (G9) fused into the prefix-scan epilogue: each row is stored
-//    straight to its image's caller index as packed 32-bit pairs.
+//    straight to its image's caller index with eight 16-byte stores.
 #include <cstdlib>
 
 #include "frame.cuh"
