@@ -25,6 +25,9 @@ r3 = rici.rici_crss_search(im[:300], h, early_exit=True)
 d = rici.rici_crss_distances(im[:40], h[:70])
 p = rici.rici_crss_pairs(im, h, torch.tensor([[0, 1], [5, 5]], dtype=torch.int64).cuda())
 r30 = rici.rici_crss_search(im30, im30)
+tag = torch.zeros(m.n_triangles, dtype=torch.uint8, device="cuda")
+tag[: m.n_triangles // 2] = 1
+cf = rici.rici_clutter_fraction(mesh, tag, o[:64], 0.3)     # f4 (clutter.cu)
 # a larger mesh: kd chunk refinement over several blocks, 4-CTA clusters with two tiles per
 # unit (>= 512 needles), and (RICI_SP_SIDE_FRAC) the side slice
 m2 = synth.bumpy_torus(80, 40, key=(8,))
@@ -36,4 +39,4 @@ r4 = rici.rici_crss_search(nee, im2)
 r5 = rici.rici_crss_search(nee, im2, early_exit=True)
 torch.cuda.synchronize()
 assert torch.equal(r1, r2) and torch.equal(r1, r3) and torch.equal(r4, r5)
-print("ok", int(r1.sum()), int(d.sum()), int(p.sum()), int(r30.sum()), int(r4.sum()))
+print("ok", int(r1.sum()), int(d.sum()), int(p.sum()), int(r30.sum()), int(r4.sum()), float(cf.sum()))
