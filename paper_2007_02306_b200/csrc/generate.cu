@@ -345,9 +345,9 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
             const float4 q0 = qa[warp][slot][0], q1 = qa[warp][slot][1], q2 = qa[warp][slot][2];
             const int k = __float_as_int(q2.y);
             float ax = q0.x, ay = q0.y, az = q0.z, bx = q0.w, by = q1.x, bz = q1.y, cx = q1.z, cy = q1.w, cz = q2.x;
+            sort3(ax, ay, az, bx, by, bz, cx, cy, cz);
             RICI_STAT(2, 1);
             RICI_STAT(3, 1);
-            sort3(ax, ay, az, bx, by, bz, cx, cy, cz);
 #if RICI_GEN_STATS
             stat_rows = max(0, min(max(__float2int_ru(cz), 0), N) - min(max(__float2int_ru(az), 0), N));
 #endif
