@@ -49,7 +49,10 @@ __device__ unsigned long long g_stats[12];
 #define RICI_STAT(i, v)
 #endif
 
-constexpr int kThreads = 256;
+#ifndef RICI_GEN_THREADS
+#define RICI_GEN_THREADS 256    // 288 / 320 (more warps per SM, fewer registers): C4 294 / 296 vs 283 ms (r2av)
+#endif
+constexpr int kThreads = RICI_GEN_THREADS;
 constexpr int kMaxK = 8;
 constexpr int kListCap = 2 * kThreads;   // superchunk survivors per batch
 constexpr int kChunkCap = 1024;          // chunk survivors per batch (multiple of kSuper)
