@@ -72,10 +72,11 @@ __device__ __forceinline__ void sort3(float &ax, float &ay, float &az, float &bx
 #undef RICI_SWAP
 }
 
+// Per-launch constants of the bin-unit frame (gen_frame): 1/delta = N/R and the row offset
+// N/2 - 1/2 (layer r at Z = r).
 struct Geometry {
-    float delta, inv_delta, half_r, r2;
-    float row_off;     // (R/2)/delta - 1/2 : row index = ceil(beta*inv_delta + row_off)
-    int n;
+    float inv_delta;
+    float row_off;
 };
 
 __device__ __forceinline__ float fast_sqrt(float x) {     // MUFU.SQRT, ~1 ulp; sqrt(0) = 0
@@ -638,11 +639,7 @@ cudaError_t launch_generate(const DeviceMesh &m, const float *d_origins, int64_t
     int64_t blocks = (n + Kt - 1) / Kt;
     // the geometry lives in the kernel's parameter bank (no per-thread recomputation)
     Geometry g;
-    g.n = N;
-    g.delta = R / (float)N;
     g.inv_delta = (float)N / R;
-    g.half_r = 0.5f * R;
-    g.r2 = R * R;
     g.row_off = 0.5f * (float)N - 0.5f;
 #define RICI_GEN_LAUNCH(KK, NN)                                                                         \
     generate_kernel<KK, NN><<<(unsigned)blocks, kThreads, smem, s>>>(m.tri, m.sphere, m.n_chunks, m.super_sphere, \
