@@ -216,9 +216,16 @@ def main():
         import torch.distributed as dist
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
         dist.init_process_group("nccl")
+    from . import rici_crss_guard_stats
+    rici_crss_guard_stats(reset=True)
     t0 = time.perf_counter()
     res = [run_scene(sc, levels, grid) for sc in range(rank, a.scenes, world)]
     wall = time.perf_counter() - t0
+    gs = rici_crss_guard_stats(reset=True)          # this rank's tensor-path guard coverage
+    guard = {"needles": gs["needles"], "haystack": gs["haystack"],
+             "haystack_outside_int8_guard": gs["haystack_outside_guard"] / max(gs["haystack"], 1),
+             "needles_outside_int8_guard": gs["needles_outside_guard"] / max(gs["needles"], 1),
+             "needles_not_2_4": gs["needles_not_2_4"] / max(gs["needles"], 1)}
     if world > 1:
         gathered = [None] * world
         dist.all_gather_object(gathered, (res, wall))
@@ -235,14 +242,14 @@ def main():
     doc = {"protocol": "clutterbox (P:379-391), synthetic tori", "levels": levels, "grid": grid,
            "scenes": a.scenes, "world_size": world, "wall_s": wall,
            "images_generated": n_img, "comparisons": n_cmp,
-           "mean_rank0_fraction": summary, "mean_clutter_fraction": clutter, "runs": res}
+           "mean_rank0_fraction": summary, "mean_clutter_fraction": clutter, "guard_rank0": guard, "runs": res}
     txt = json.dumps(doc, indent=1, default=str)
     if a.out:
         with open(a.out, "w") as f:
             f.write(txt)
     print(json.dumps({"scenes": a.scenes, "levels": [levels[0], levels[-1]], "world_size": world, "wall_s": wall,
                       "images_per_s": n_img / wall, "comparisons_per_s": n_cmp / wall,
-                      "mean_rank0_fraction": summary, "mean_clutter_fraction": clutter}))
+                      "mean_rank0_fraction": summary, "mean_clutter_fraction": clutter, "guard_rank0": guard}))
 
 
 if __name__ == "__main__":

@@ -1,3 +1,4 @@
+# smoke, pytest -m gpu, the bench and its ncu launch list in one gpurun call
 set -x
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke rc=$?
