@@ -335,6 +335,19 @@ def test_guard_fallback_many_haystack_images(rici, oracle_mod):
     assert np.array_equal(r.astype(np.uint32), oracle_mod.ranks(A, H))
 
 
+def test_more_needles_than_haystack(rici, oracle_mod):
+    """Tensor path with more needle rows than haystack rows (the feature pass is then one
+    launch in which every row stages both images): count_below of 700 needles (2:4 and dense
+    subsets, one guard break) against 300 haystack images, exact against the oracle."""
+    rng = np.random.default_rng(77)
+    H = _mixed_images(rng, 300, 6, 2, 40)
+    A = np.concatenate([H, _mixed_images(rng, 400, 6, 1, 300)])
+    D = oracle_mod.crss_matrix(A, H)
+    thr = D[np.arange(700), rng.integers(0, 300, 700)].copy()
+    got = rici.rici_crss_count_below(_dev(A), _dev(H), torch.from_numpy(thr.view(np.int64)).to(DEV))
+    assert np.array_equal(got.cpu().numpy().astype(np.int64), (D < thr[:, None]).sum(1))
+
+
 def test_search_captured_in_cuda_graph(rici, oracle_mod):
     """No host synchronisation anywhere in rici_crss_search / count_below (tensor path with the
     device-sized dense subset and guard fallback): the calls capture into a CUDA graph, and the
