@@ -281,6 +281,38 @@ def extra_c3(rici, torch, dev, stream, flush, reps=3):
                         "vertices", "ms": ms, "images_per_s": m.n_vertices / (ms / 1e3), "reps": reps}
 
 
+def extra_gen_series(rici, torch, dev, stream, flush, levels=(1, 2, 4, 6, 8), reps=2):
+    """Generation rate vs scene triangle count (fig:results_generation_rate): the C3
+    clutterbox recipe with k objects (k = 10 is C3 itself, c3_construction), RICI at all
+    vertices; mesh staging + rici_generate, device-resident, CUDA events."""
+    import synth
+    pts = []
+    for k in levels:
+        cfg = synth.config_c3(n_obj=k)
+        m = cfg["mesh"]
+        v, t, o = (torch.from_numpy(x).to(dev) for x in (m.vertices, m.indices, cfg["origins"]))
+        out = torch.empty((m.n_vertices, 64, 64), dtype=torch.int16, device=dev)
+        ts = []
+        for it in range(reps + 1):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            mesh = rici.rici_create_mesh(v, t)
+            rici.rici_generate(mesh, o, cfg["R"], cfg["N"], out=out)
+            b.record(stream)
+            mesh.destroy()
+            torch.cuda.synchronize()
+            if it:
+                ts.append(a.elapsed_time(b))
+        ms = float(np.mean(ts))
+        pts.append({"objects": k, "triangles": int(m.n_triangles), "images": int(m.n_vertices), "ms": ms,
+                    "images_per_s": m.n_vertices / (ms / 1e3)})
+        del out, v, t, o
+    return {"workload": "C3 recipe (bumpy tori 316x158, clutterbox side 3) with k objects, RICI at all vertices; "
+                        "the k = 10 point is c3_construction, the 2,007,040-triangle point the step's construction",
+            "points": pts, "reps": reps}
+
+
 def extra_c2(rici, torch, dev, stream, flush, reps=5, simt=True):
     """The round-1 C2 step (BASELINE configs[1]): mesh + RICI at all 34,848 vertices of the
     264x132 torus + CRSS self-search (1.21e9 comparisons); and the SIMT CRSS path on it."""
@@ -571,6 +603,7 @@ def run_gpu(args):
         del hay
         torch.cuda.empty_cache()
         extras["c3_construction"] = extra_c3(rici, torch, dev, stream, flush)
+        extras["generation_rate_series"] = extra_gen_series(rici, torch, dev, stream, flush)
         extras["c2_step"] = extra_c2(rici, torch, dev, stream, flush)
     images = n_ref + n_sc
     line = {"metric": METRIC, "value": images / (step_ms / 1e3), "unit": "images/s", "n_gpus": world,
