@@ -58,9 +58,8 @@ constexpr int kListCap = 2 * kThreads;   // superchunk survivors per batch
 constexpr int kChunkCap = 1024;          // chunk survivors per batch (multiple of kSuper)
 
 // Bin indices in the bin-unit frame (rasterise_triangle): the first row r with Z_r = r >= v is
-// ceil(v), the first column whose circle (radius c + 1/2) is at or beyond v is ceil(v - 1/2);
-// cvt.rpi.s32.f32 (__float2int_ru) is ceil with saturation (NaN -> 0).  Exact ties are fragile
-// pixels (G5).
+// ceil(v), the first column whose circle (radius c + 1/2) is at or beyond v is ceil(v - 1/2),
+// both clamped to [0, N] and computed as kMagic sums (below).  Exact ties are fragile pixels (G5).
 
 // Stable sort of three vertices by z (a three-stage network; equal z keep their order).
 __device__ __forceinline__ void sort3(float &ax, float &ay, float &az, float &bx, float &by,
@@ -115,6 +114,12 @@ __device__ __forceinline__ float mul_sat(float a, float b) {     // FMUL.SAT: cl
     return r;
 }
 
+// Bin indices without F2I / I2F / FRND (XU ops; C4 283.3 -> 279.9 ms, images identical, r2bl-r2bm):
+// ceil(v) + 1.5 * 2^23 is v + 1.5 * 2^23 rounded UP, exactly for |v| < 2^22 (unit ulp there), so
+// the float's bits are ceil(v) + 0x4B400000 and the float minus the magic is ceil(v); positive
+// floats order like their bits (negative ones as signed integers), so clamps need no conversion.
+constexpr float kMagic = 12582912.f;
+constexpr int kMagicBits = 0x4B400000;
 #ifndef RICI_GEN_RED_MODE
 #define RICI_GEN_RED_MODE 1     // C4 341 -> 337 ms against the branch on an empty range (r2d)
 #endif
@@ -128,10 +133,15 @@ __device__ __forceinline__ void rasterise_triangle(unsigned acc, int n_rt,
                                                    float by, float bz, float cx, float cy,
                                                    float cz) {
     const int N = NC ? NC : n_rt;
-    const int r_lo = min(max(__float2int_ru(az), 0), N);     // first row with Z_r >= z_a
-    const int r_hi = min(max(__float2int_ru(cz), 0), N);
-    if (r_lo >= r_hi) { RICI_STAT(8, 1); return; }
+    // first row with Z_r >= z_a / z_c, clamped to [0, N], without F2I / I2F (kMagic)
+    const float2 rc = __fadd2_ru(f2(az, cz), f2(kMagic, kMagic));
+    const int b_lo = min(max(__float_as_int(rc.x), kMagicBits), kMagicBits + N);
+    const int b_hi = min(max(__float_as_int(rc.y), kMagicBits), kMagicBits + N);
+    if (b_lo >= b_hi) { RICI_STAT(8, 1); return; }
+    const int r_lo = b_lo - kMagicBits;
+    const float2 rzr = __fadd2_rn(f2(__int_as_float(b_lo), __int_as_float(b_hi)), f2(-kMagic, -kMagic));
 #if RICI_GEN_STATS
+    const int r_hi = b_hi - kMagicBits;
     bool stat_emitted = false;
 #endif
     RICI_STAT(4, r_hi - r_lo);
@@ -142,9 +152,14 @@ __device__ __forceinline__ void rasterise_triangle(unsigned acc, int n_rt,
                  BC = f2(cx - bx, cy - by);
     const float2 half = f2(-0.5f, -0.5f);
     const unsigned row_step = 4u * (unsigned)(N + 1);
-    unsigned row = acc + row_step * (unsigned)r_lo;
-    const float rz_hi = (float)r_hi;
-    for (float rz = (float)r_lo; rz < rz_hi; rz += 1.f, row += row_step) {
+    // Column indices without F2I (an XU op): the bits of v + kMagic rounded up are ceil(v) +
+    // 0x4B400000 (larger v land above the clamp), and the shared-window address 4 * bits +
+    // (row - 4 * 0x4B400000) wraps to the row's column: bitwise the indices of min(ceil(v), N)
+    // (__float2int_ru) for every finite v >= -1/2.
+    const unsigned cap = (unsigned)kMagicBits + (unsigned)N;
+    unsigned row = acc + row_step * (unsigned)r_lo - 4u * (unsigned)kMagicBits;
+    const float rz_hi = rzr.y;
+    for (float rz = rzr.x; rz < rz_hi; rz += 1.f, row += row_step) {
         // Step 1: E0 on the long edge (a,c), E1 on (a,b) below / (b,c) above the middle vertex.
         const float t = mul_sat(rz - az, i_ac);
         const float2 e0 = __ffma2_rn(f2(t, t), AC, A);
@@ -160,17 +175,17 @@ __device__ __forceinline__ void rasterise_triangle(unsigned acc, int n_rt,
         // Steps 3-4: distances of E0, E1 from the axis; single range [min, max).  Column c's
         // circle (radius c + 1/2 in bin units) is the first at or beyond v at ceil(v - 1/2).
         const float r0 = fast_sqrt(fmaf(e0.x, e0.x, e0.y * e0.y)), r1 = fast_sqrt(fmaf(e1.x, e1.x, e1.y * e1.y));
-        const float2 cf = __fadd2_rn(f2(fminf(r0, r1), fmaxf(r0, r1)), half);
-        const int c_min = min(__float2int_ru(cf.x), N), c_max = min(__float2int_ru(cf.y), N);
+        const float2 cf = __fadd2_ru(__fadd2_rn(f2(fminf(r0, r1), fmaxf(r0, r1)), half), f2(kMagic, kMagic));
+        const unsigned c_min = min(__float_as_uint(cf.x), cap), c_max = min(__float_as_uint(cf.y), cap);
         // Steps 5-6: double range [|C|, min) iff the x signs differ (x = 0 non-negative);
         // |C| = |rotated y| = |D x E0| / |D|.  Single: +1 at c_min, -1 at c_max.  Double:
         // +2 at c_c, -1 at c_min, -1 at c_max.  Empty ranges (also a zero-length slice, whose
         // r0 = r1 and de0 = 0) cancel at one address; they are predicated off.
         const bool dbl = de0 < 0.f && de0 + l2 >= 0.f;
-        int c_lo = c_min;
+        unsigned c_lo = c_min;
         if (dbl) {
             const float y = fmaf(d.x, e0.y, -d.y * e0.x) * rsqrtf(l2);
-            c_lo = min(min(__float2int_ru(fabsf(y) - 0.5f), N), c_min);
+            c_lo = min(__float_as_uint(__fadd_ru(fabsf(y) - 0.5f, kMagic)), c_min);
         }
         const bool emit = c_lo != c_max;                  // something in [c_lo, c_max)
         (void)emit;
@@ -483,9 +498,11 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
                         project_z(f, v, pp, p2, z);
                         float zlo = fminf(z[0], fminf(z[1], z[2])), zhi = fmaxf(z[0], fmaxf(z[1], z[2]));
                         // beta-extent test: a layer Z = r in [zlo, zhi) with 0 <= r < N,
-                        // i.e. the first row at or above max(zlo, 0) lies below min(zhi, N)
-                        // (one FRND.CEIL; C4 289.4 -> 286.4 ms against ceil-to-int and clamps, r2x)
-                        bool keep = ceilf(fmaxf(zlo, 0.f)) < fminf(zhi, (float)N);
+                        // i.e. the first row at or above max(zlo, 0) lies below min(zhi, N); for an
+                        // integer k, k < b iff k < ceil(b), so both sides are ceilings, taken as
+                        // kMagic sums by one FADD2.RP (float tests: C4 289.4 -> 286.4 ms, r2x)
+                        const float2 cb = __fadd2_ru(f2(fmaxf(zlo, 0.f), fminf(zhi, (float)N)), f2(kMagic, kMagic));
+                        bool keep = cb.x < cb.y;
                         if (keep) {
                             project_xy(f, pp, p2, x, y);
                             keep = alpha_box_hits(x, y, (float)(N * N));
