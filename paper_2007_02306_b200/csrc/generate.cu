@@ -121,14 +121,14 @@ __device__ __forceinline__ float mul_sat(float a, float b) {     // FMUL.SAT: cl
 constexpr float kMagic = 12582912.f;
 constexpr int kMagicBits = 0x4B400000;
 #ifndef RICI_GEN_RED_MODE
-#define RICI_GEN_RED_MODE 1     // C4 341 -> 337 ms against the branch on an empty range (r2d)
+#define RICI_GEN_RED_MODE 3     // 1: per-row (v1, v2) selects (r2d: C4 341 -> 337 ms against 0, a branch)
 #endif
 
 // All coordinates here are in BIN units (DESIGN.md 6.1 "bin-unit frame"): x, y scaled by
 // 1/delta = N/R, and Z = z/delta + N/2 - 1/2, so layer r lies at Z = r exactly (beta_r =
 // (r + 1/2) delta - R/2, G4), column c's circle at radius c + 1/2, and the support radius is N.
 template <int NC>
-__device__ __forceinline__ void rasterise_triangle(unsigned acc, int n_rt,
+__device__ __forceinline__ void rasterise_triangle(unsigned acc, int n_rt, int two, int neg1,
                                                    float ax, float ay, float az, float bx,
                                                    float by, float bz, float cx, float cy,
                                                    float cz) {
@@ -193,7 +193,17 @@ __device__ __forceinline__ void rasterise_triangle(unsigned acc, int n_rt,
 #if RICI_GEN_STATS
         stat_emitted |= emit;
 #endif
-#if RICI_GEN_RED_MODE == 1
+#if RICI_GEN_RED_MODE == 3
+        // unconditional and constant: +2 at c_lo, -1 at c_min, -1 at c_max.  A single range has
+        // c_lo = c_min, where +2 - 1 leaves its +1; an empty range cancels in place.  The
+        // constants sit in registers the compiler cannot rematerialise (two = 2, neg1 = -1,
+        // derived from a kernel parameter) instead of a move per row: layer loop 56 -> 52
+        // instructions, C4 279.8 -> 277.9 ms, C3 86.7 -> 85.8 ms, images identical (r2bn)
+        red_shared(row + 4u * (unsigned)c_lo, two);
+        red_shared(row + 4u * (unsigned)c_min, neg1);
+        red_shared(row + 4u * (unsigned)c_max, neg1);
+    }
+#elif RICI_GEN_RED_MODE == 1
         // unconditional: +v1 at c_lo, +v2 at c_min, -1 at c_max with (v1, v2) = (2, -1) for a
         // double range and (1, 0) for a single one; an empty range cancels in place
         red_shared(row + 4u * (unsigned)c_lo, dbl ? 2 : 1);
@@ -296,6 +306,7 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
 
     int *acc = reinterpret_cast<int *>(smem_raw);        // [K][N][N+1] difference arrays
     const unsigned acc_s = (unsigned)__cvta_generic_to_shared(acc);
+    const int c_two = 2 + (N >> 31), c_neg1 = -1 - (N >> 31);   // 2 and -1 (N > 0), opaque to ptxas
     if (NC) N = NC;                                      // N = 64: compile-time bin geometry
     const int img_words = N * (N + 1);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -370,7 +381,8 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
 #if RICI_GEN_STATS
             stat_rows = max(0, min(max(__float2int_ru(cz), 0), N) - min(max(__float2int_ru(az), 0), N));
 #endif
-            rasterise_triangle<NC>(acc_s + 4u * (unsigned)(k * img_words), N, ax, ay, az, bx, by, bz, cx, cy, cz);
+            rasterise_triangle<NC>(acc_s + 4u * (unsigned)(k * img_words), N, c_two, c_neg1, ax, ay, az, bx, by, bz,
+                                   cx, cy, cz);
         }
 #if RICI_GEN_STATS
         {
