@@ -43,7 +43,7 @@ namespace rici {
 namespace {
 
 #if RICI_GEN_STATS   // tuning builds only: event counters read by rici_debug_gen_stats
-__device__ unsigned long long g_stats[12];
+__device__ unsigned long long g_stats[13];
 #define RICI_STAT(i, v) atomicAdd(&g_stats[i], (unsigned long long)(v))
 #else
 #define RICI_STAT(i, v)
@@ -120,6 +120,9 @@ __device__ __forceinline__ float mul_sat(float a, float b) {     // FMUL.SAT: cl
 // floats order like their bits (negative ones as signed integers), so clamps need no conversion.
 constexpr float kMagic = 12582912.f;
 constexpr int kMagicBits = 0x4B400000;
+#ifndef RICI_GEN_INSIDE
+#define RICI_GEN_INSIDE 1
+#endif
 #ifndef RICI_GEN_RED_MODE
 #define RICI_GEN_RED_MODE 3     // 1: per-row (v1, v2) selects (r2d: C4 341 -> 337 ms against 0, a branch)
 #endif
@@ -439,7 +442,16 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
                                 float ex = s4.x - f.sx, ey = s4.y - f.sy, ez = s4.z - f.sz;
                                 float b = fmaf(f.czx, ex, fmaf(f.czy, ey, f.czz * ez));
                                 float a2 = fmaxf(ex * ex + ey * ey + ez * ez - b * b, 0.f);
-                                if (fabsf(b) <= hb && a2 <= ra * ra) kbits |= 1u << k;
+                                if (fabsf(b) <= hb && a2 <= ra * ra) {
+                                    kbits |= 1u << k;
+#if RICI_GEN_INSIDE
+                                    // the whole chunk within radius R of the axis: every triangle's
+                                    // (T_x, T_y) box meets the support disk, so its alpha test is
+                                    // skipped (it is an exact skip, so a loose flag only costs work)
+                                    const float ri = R - s4.w - pad;
+                                    if (K <= 4 && ri > 0.f && a2 <= ri * ri) kbits |= 1u << (4 + k);
+#endif
+                                }
                             }
                         }
                     }
@@ -459,8 +471,8 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
                 // layer Z = r lie in [z_min, z_max)?  then the alpha box; survivors go to the
                 // warp's ring with their projected vertices
                 auto process = [&](const unsigned ent, const float *v) {
-                    const unsigned kmask = ent & 0xffu;
-                    if (lane == 0) { RICI_STAT(0, 1); RICI_STAT(1, __popc(kmask)); }
+                    const unsigned kmask = ent & (K <= 4 && RICI_GEN_INSIDE ? 0xfu : 0xffu);
+                    if (lane == 0) { RICI_STAT(0, 1); RICI_STAT(1, __popc(kmask)); RICI_STAT(12, __popc((ent >> 4) & 0xfu)); }
     #if RICI_GEN_STATS
                         {   // finer culls, counted only: the 8-triangle sub-chunk's sphere and the triangle's
                             // own sphere against each tested image's support cylinder (stats 10, 11)
@@ -517,7 +529,10 @@ generate_kernel(const float *__restrict__ tri, const float4 *__restrict__ sphere
                         bool keep = cb.x < cb.y;
                         if (keep) {
                             project_xy(f, pp, p2, x, y);
-                            keep = alpha_box_hits(x, y, (float)(N * N));
+#if RICI_GEN_INSIDE
+                            if (!(K <= 4 && ((ent >> (4 + k)) & 1u)))   // warp-uniform
+#endif
+                                keep = alpha_box_hits(x, y, (float)(N * N));
                         }
                         const unsigned m = __ballot_sync(0xffffffffu, keep);
                         if (keep) {
@@ -693,8 +708,8 @@ cudaError_t launch_generate(const DeviceMesh &m, const float *d_origins, int64_t
 #if RICI_GEN_STATS
 extern "C" __attribute__((visibility("default"))) int rici_debug_gen_stats(unsigned long long *out, int reset) {
     cudaDeviceSynchronize();
-    cudaMemcpyFromSymbol(out, rici::g_stats, sizeof(unsigned long long) * 12);
-    if (reset) { unsigned long long z[12] = {}; cudaMemcpyToSymbol(rici::g_stats, z, sizeof(z)); }
+    cudaMemcpyFromSymbol(out, rici::g_stats, sizeof(unsigned long long) * 13);
+    if (reset) { unsigned long long z[13] = {}; cudaMemcpyToSymbol(rici::g_stats, z, sizeof(z)); }
     return 0;
 }
 #endif

@@ -23,13 +23,14 @@ else:
     cfg = synth.config_c2(); m = cfg["mesh"]
 mesh = rici.rici_create_mesh(torch.from_numpy(m.vertices).cuda(), torch.from_numpy(m.indices).cuda())
 o = torch.from_numpy(cfg["origins"]).cuda()
-buf = (ctypes.c_ulonglong * 12)()
+buf = (ctypes.c_ulonglong * 13)()
 rici.rici_generate(mesh, o, 0.3, 64); lib.rici_debug_gen_stats(buf, 1)
 rici.rici_generate(mesh, o, 0.3, 64); lib.rici_debug_gen_stats(buf, 1)
 n = m.n_vertices
 names = ["chunk_visits", "chunk_image_pairs", "queued_pairs", "alpha_pass_pairs", "rows", "segments",
          "layer_loop_warp_iterations", "drains", "pairs_without_layer", "pairs_without_segment",
-         "pairs_subchunk8_sphere_in_cylinder", "pairs_triangle_sphere_in_cylinder"]
+         "pairs_subchunk8_sphere_in_cylinder", "pairs_triangle_sphere_in_cylinder",
+         "chunk_image_pairs_inside_radius"]
 res = {k: buf[i] / n for i, k in enumerate(names)}
 res["triangle_pairs_tested"] = res["chunk_image_pairs"] * 32
 print(json.dumps({"per_image": res, "images": n}))
