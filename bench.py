@@ -46,10 +46,23 @@ WORKLOAD = ("C4 (BASELINE configs[3]): needles = RICI 64x64 at the 100,352 verti
             "search 100,352 x 1,003,520 = 1.007e11 comparisons, ranks of i <-> i")
 
 
-def ncu_metric(kernel, metric):
-    """A metric of `kernel` from the newest committed ncu summary (profiles/r*_ncu_summary.txt)."""
+def ncu_summaries():
+    """Committed ncu summaries, the current one (named in profiles/ncu_current.txt) first, then
+    the others newest name first."""
     import glob
-    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_summary.txt")), reverse=True):
+    paths = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_summary*.txt")), reverse=True)
+    cur = os.path.join(ROOT, "profiles", "ncu_current.txt")
+    if os.path.exists(cur):
+        first = os.path.join(ROOT, "profiles", open(cur).read().strip())
+        if first in paths:
+            paths.remove(first)
+            paths.insert(0, first)
+    return paths
+
+
+def ncu_metric(kernel, metric):
+    """A metric of `kernel` from the current committed ncu summary (ncu_summaries())."""
+    for path in ncu_summaries():
         cur = None
         for line in open(path):
             if line.startswith("== "):
@@ -62,9 +75,8 @@ def ncu_metric(kernel, metric):
 def ncu_traffic(kernel):
     """dram__bytes_read.sum + dram__bytes_write.sum of `kernel` per launch, from the newest
     committed `ncu --set full` summary under profiles/; None if absent."""
-    import glob
     scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
-    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_summary.txt")), reverse=True):
+    for path in ncu_summaries():
         cur, tot, seen = None, 0.0, 0
         for line in open(path):
             if line.startswith("== "):
