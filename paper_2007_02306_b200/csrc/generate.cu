@@ -54,8 +54,14 @@ __device__ unsigned long long g_stats[13];
 #endif
 constexpr int kThreads = RICI_GEN_THREADS;
 constexpr int kMaxK = 8;
-constexpr int kListCap = 2 * kThreads;   // superchunk survivors per batch
-constexpr int kChunkCap = 1024;          // chunk survivors per batch (multiple of kSuper)
+#ifndef RICI_GEN_LIST_CAP
+#define RICI_GEN_LIST_CAP (2 * RICI_GEN_THREADS)
+#endif
+#ifndef RICI_GEN_CHUNK_CAP
+#define RICI_GEN_CHUNK_CAP 3072         // fewer level-3 batches, fewer imbalanced barriers: C4 272.9 -> 270.0 ms (r2cs)
+#endif
+constexpr int kListCap = RICI_GEN_LIST_CAP;    // superchunks tested per level-1 batch
+constexpr int kChunkCap = RICI_GEN_CHUNK_CAP;  // chunk survivors per batch (multiple of kSuper)
 
 // Bin indices in the bin-unit frame (rasterise_triangle): the first row r with Z_r = r >= v is
 // ceil(v), the first column whose circle (radius c + 1/2) is at or beyond v is ceil(v - 1/2),
