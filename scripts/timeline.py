@@ -1,6 +1,6 @@
 """Kernel timeline of one C2 step (create_mesh + generate + search) from the torch profiler
 (CUPTI activity records: start/end of every kernel on every stream) -- finds gaps and overlap.
-WORKLOAD=c4: only the C4 search (images generated first, outside the profile)."""
+WORKLOAD=c4: only the C4 search (images generated first, outside the profile); RANK=1 in rank mode."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -28,7 +28,7 @@ elif os.environ.get("WORKLOAD") == "c4":
     ranks = torch.empty(gen[0].shape[0], dtype=torch.int32, device="cuda")
 
     def step():
-        rici.rici_crss_search(gen[0], gen[1], out=ranks)
+        rici.rici_crss_search(gen[0], gen[1], out=ranks, early_exit=os.environ.get("RANK") == "1")
 else:
     cfg = synth.config_c2(); m = cfg["mesh"]
     v, t, o = (torch.from_numpy(x).cuda() for x in (m.vertices, m.indices, cfg["origins"]))
